@@ -1,0 +1,176 @@
+/*
+ * otn_b200.h — C-ABI of the B200-native truncated-Newton EOT solver.
+ *
+ * This is the drop-in boundary for the reference's hot path (otnewton 0.1.0,
+ * arXiv 2504.02067).  Each entry point replaces one operator of the
+ * reference's internal operator seam; the reference interface
+ * it replaces is cited as  file:line  relative to /root/reference/pkg/src/otnewton.
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers to float64 data owned by the
+ *    caller (e.g. torch CUDA tensors).  No torch types cross this boundary.
+ *  - n x n matrices (cost C, plan P) are row-major with leading dimension
+ *    `ld` (fixed at otn_create; a multiple of 32, padding columns ignored on
+ *    read and written as 0 on write).  Vectors have n entries.
+ *  - Calls are stream-ordered on the context's stream.  Only calls that return
+ *    host scalars (pointer arguments named host_*) synchronize the stream.
+ *  - Return value: OTN_OK, an OTN_ERR_* failure, or an OTN_ST_* solver status
+ *    that the host maps onto the reference's exception taxonomy
+ *    (errors.py:11-65) with the same diagnostics.
+ *  - A context is single-owner and not thread-safe, like the reference's
+ *    DualState (dual.py:22-28).
+ *  - Reductions are fixed-order trees without floating-point atomics: results
+ *    are bit-reproducible run to run.
+ */
+#ifndef OTN_B200_H
+#define OTN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OTN_ABI_VERSION 1
+
+enum otn_status {
+  OTN_OK = 0,
+  OTN_ERR_CUDA = 1,              /* CUDA runtime failure; see otn_last_error()            */
+  OTN_ERR_ARG = 2,               /* bad argument                                          */
+  OTN_ST_PLAN_OVERFLOW = 10,     /* PlanOverflowError   (_kernels.py:55-58)               */
+  OTN_ST_NONPOSITIVE_SUMS = 11,  /* ConditioningError   (newton.py:76-77)                 */
+  OTN_ST_BREAKDOWN = 12,         /* ConditioningError   (newton.py:155-156)               */
+  OTN_ST_PRECOND = 13,           /* ConditioningError   (newton.py:137-139)               */
+  OTN_ST_NONCONVERGENCE = 14,    /* NonconvergenceError (newton.py:168-172), best = x     */
+  OTN_ST_STAGNATION = 15,        /* StagnationError     (newton.py:202-205)               */
+  OTN_ST_DOMAIN = 16             /* DomainError         (core.py:47-50)                   */
+};
+
+/* Vector ops for otn_vec (element-wise, operand order as in the reference). */
+enum otn_vec_op {
+  OTN_VEC_ADD_SUB = 0,  /* out = (a + b) - c        projector.py:146, dual.py:189          */
+  OTN_VEC_AXPY = 1,     /* out = a + s*b            projector.py:234                        */
+  OTN_VEC_STEP_V = 2,   /* out = (a + s*b) + (c - d) projector.py:235                       */
+  OTN_VEC_EXTRAP = 3,   /* out = a + s*(a - b)      driver.py:170-175                       */
+  OTN_VEC_EXP = 4,      /* out = exp(a)             dual.py:134-138                         */
+  OTN_VEC_GRAD = 5      /* out = exp(a) - b         projector.py:176                        */
+};
+
+/* Reductions for otn_reduce; results go to host_out[0..1]. */
+enum otn_reduce_op {
+  OTN_RED_ROW_STATS = 0, /* [sum|exp(a)-b|, sum b*b/exp(a)]; flags: exp(a)<=0 -> 1, b<0 -> 2
+                            (projector.py:176-177, core.py:42-52)                         */
+  OTN_RED_GRAD_L1 = 1,   /* [sum|exp(a)-b|, sum|exp(c)-d|]   dual.py:142-148              */
+  OTN_RED_SUM_EXP = 2,   /* [sum exp(a)]                      projector.py:122-126         */
+  OTN_RED_DOT = 3,       /* [sum a*b]                         dual.py:150-153              */
+  OTN_RED_L1 = 4         /* [sum |a|]                                                      */
+};
+
+typedef struct otn_ctx otn_ctx;
+
+/* Outcome of otn_newton / otn_pcg (host copy of the device record). */
+typedef struct {
+  int32_t status;      /* OTN_OK or OTN_ST_*                                         */
+  int32_t pcg_calls;   /* pcg_solve calls made (op tally: diag_prc on the first)   */
+  int64_t cg_iters;    /* newton: total CG iterations; pcg: iterations             */
+  int64_t hvps;        /* F(rho)x products with rho != 0 (2 matvec passes each)    */
+  double rho_final;    /* newton: discount of the last PCG call (newton.py:209)    */
+  double resid_l1;     /* newton: undiscounted residual L1 (newton.py:199-201)     */
+  double slope;        /* newton: -(grad_u . d_u)  (projector.py:205)              */
+  double diag_rho;     /* NonconvergenceError diagnostics: rho                     */
+  double diag_resid;   /* NonconvergenceError diagnostics: residual_l1             */
+} otn_solve_result;
+
+/* ---- context ---------------------------------------------------------- */
+int otn_abi_version(void);
+const char* otn_last_error(void);
+/* Allocate the device workspace for problems of size n (leading dim ld). */
+int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream);
+int otn_destroy(otn_ctx* ctx);
+int otn_set_stream(otn_ctx* ctx, void* stream);
+/* out4 = {n, ld, persistent-solver CTAs, workspace bytes} */
+int otn_info(const otn_ctx* ctx, int64_t* out4);
+/* Synchronize and copy the four device status flags to the host:
+ * [0] plan overflow, [1] nonpositive sums, [2] reduce domain, [3] rounding. */
+int otn_read_flags(otn_ctx* ctx, int* host4);
+
+/* ---- log-domain reductions (K1, K2, K3) --------------------------------- */
+/* out_i = outer_i + LSE_j(neg_gamma*C_ij + inner_j); outer may be NULL (0.0).
+ * Replaces _kernels.py:22-42 log_plan_row_sums(K, u, v) with K = -gamma*C
+ * formed in registers (same single rounding as dual.py:74).               */
+int otn_lse_rows(otn_ctx* ctx, const double* C, double neg_gamma, const double* outer,
+                 const double* inner, double* out);
+/* out_j = outer_j + LSE_i(neg_gamma*C_ij + inner_i) — the column reduction
+ * log_plan_row_sums(K^T, v, u) of dual.py:91-102 / dual.py:186-194.  With
+ * symmetric != 0 the rows of C are read instead (K^T aliases K, dual.py:80-88). */
+int otn_lse_cols(otn_ctx* ctx, const double* C, int symmetric, double neg_gamma,
+                 const double* outer, const double* inner, double* out);
+/* v_j = log_c_j - LSE_i(neg_gamma*C_ij + u_i)   (rebalance_columns, dual.py:179-184) */
+int otn_rebalance_cols(otn_ctx* ctx, const double* C, int symmetric, double neg_gamma,
+                       const double* log_c, const double* u, double* v_out);
+/* Line-search objective: out_j = (v + alpha*dv)_j + LSE_i(neg_gamma*C_ij + (u + alpha*du)_i)
+ * and *host_mass = sum_j exp(out_j) (overflow -> inf).
+ * Replaces dual.py:171-175 trial_log_col_sums + projector.py:122-126 _mass. */
+int otn_trial_cols(otn_ctx* ctx, const double* C, int symmetric, double neg_gamma,
+                   const double* u, const double* du, const double* v, const double* dv,
+                   double alpha, double* out, double* host_mass);
+
+/* ---- plan (K4 + K5) ------------------------------------------------------ */
+/* P_ij = exp((neg_gamma*C_ij + v_j) + u_i).  If icP != NULL also
+ * mu_i = (sum_j P_ij^2 icP_j) / rP_i (the Jacobi diagonal, K5 fused).
+ * Overflow (an exponent > 700) sets a device flag that the next otn_newton /
+ * otn_pcg reports as OTN_ST_PLAN_OVERFLOW; when host_overflow != NULL the call
+ * synchronizes and returns the flag.  Replaces _kernels.py:45-61
+ * materialize_plan and newton.py:107-112 diag_prc / _kernels.py:64-74.     */
+int otn_materialize(otn_ctx* ctx, const double* C, double neg_gamma, const double* u,
+                    const double* v, double* P, const double* icP, const double* rP,
+                    double* mu, int* host_overflow);
+/* rP = exp(log_rP), cP = exp(log_cP), icP = 1/cP; nonpositive sums set the
+ * OTN_ST_NONPOSITIVE_SUMS flag (DiscountedSystem.__init__, newton.py:72-90). */
+int otn_system_prep(otn_ctx* ctx, const double* log_rP, const double* log_cP, double* rP,
+                    double* cP, double* icP, int* host_bad);
+/* (P*P) @ w   (_kernels.py:64-74) */
+int otn_square_matvec(otn_ctx* ctx, const double* P, const double* w, double* out);
+
+/* ---- Hessian-vector products (K6, K7) ------------------------------------ */
+int otn_matvec(otn_ctx* ctx, const double* P, const double* x, double* out);   /* newton.py:43-48  */
+int otn_rmatvec(otn_ctx* ctx, const double* P, const double* x, double* out);  /* newton.py:51-56  */
+/* out = rP*d - rho*P((P^T d)/cP)   (newton.py:100-105) */
+int otn_apply_F(otn_ctx* ctx, const double* P, const double* rP, const double* cP, double rho,
+                const double* d, double* out);
+/* out = (P^T d)/cP   (newton.py:96-98) */
+int otn_apply_pc(otn_ctx* ctx, const double* P, const double* cP, const double* d, double* out);
+
+/* ---- device-resident solvers (K8 + the CG / Newton loops) ----------------- */
+/* Jacobi-PCG on F(rho) x = b to L1 recurrence residual <= tol, x in/out
+ * (has_x0 = 0: start from zero).  One persistent cooperative launch, no host
+ * round trip per iteration.  Replaces newton.py:123-172 pcg_solve.          */
+int otn_pcg(otn_ctx* ctx, const double* P, const double* rP, const double* cP, const double* mu,
+            double rho, const double* b, double tol, double* x, int has_x0, int64_t max_iters,
+            otn_solve_result* host_res);
+/* Annealed truncated-Newton direction (newton.py:175-210) for gradient g,
+ * forcing eta, starting discount rho0; writes d_u and, if d_v != NULL, the
+ * back-substitution d_v = -(P^T d_u)/cP plus the slope -(g.d_u)
+ * (projector.py:196-205).  One persistent cooperative launch.               */
+int otn_newton(otn_ctx* ctx, const double* P, const double* rP, const double* cP,
+               const double* mu, const double* g, double eta, double rho0, int zero_init,
+               int64_t max_iters, double* d_u, double* d_v, otn_solve_result* host_res);
+
+/* ---- projector / driver vector work ------------------------------------- */
+int otn_vec(otn_ctx* ctx, int op, double s, const double* a, const double* b, const double* c,
+            const double* d, double* out);
+int otn_reduce(otn_ctx* ctx, int op, const double* a, const double* b, const double* c,
+               const double* d, double* host_out, int* host_flags);
+/* Round P onto U(r, c) in place and return host_out = {<P, C>, deficit}
+ * (driver.py:178-208 round_plan + driver.py:306-310 vdot).  C may be NULL
+ * (primal cost skipped).  host_flags: 1 = negative entry (DomainError),
+ * 2 = zero total mass (DegenerateInputError).                               */
+int otn_round_plan(otn_ctx* ctx, double* P, const double* C, const double* r, const double* c,
+                   double* host_out, int* host_flags);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OTN_B200_H */

@@ -1,0 +1,167 @@
+"""Device plumbing: contexts, padded device buffers, the device-resident cost.
+
+PyTorch is used only for device memory, streams and host<->device copies; all
+arithmetic on the solver path runs in the C-ABI library (``_lib``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import DeviceError
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_cuda(device=None):
+    t = torch()
+    if not t.cuda.is_available():
+        raise DeviceError("a CUDA device is required: this package has no CPU fallback")
+    if device is None:
+        device = t.device("cuda", t.cuda.current_device())
+    device = t.device(device)
+    if device.type != "cuda":
+        raise DeviceError(f"expected a CUDA device, got {device}")
+    if device.index is None:
+        device = t.device("cuda", t.cuda.current_device())
+    return device
+
+
+def round_up(n, k=32):
+    return (n + k - 1) // k * k
+
+
+def vptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def is_tensor(x):
+    return type(x).__module__.startswith("torch") and hasattr(x, "data_ptr")
+
+
+class Context:
+    """One C-ABI context (device workspace) per (device, n)."""
+
+    _cache = {}
+
+    def __init__(self, n, device):
+        self.lib = _lib.load()
+        self.n = int(n)
+        self.ld = round_up(self.n, 32)
+        self.device = device
+        t = torch()
+        with t.cuda.device(device):
+            stream = t.cuda.current_stream(device).cuda_stream
+            h = ctypes.c_void_p()
+            rc = self.lib.otn_create(ctypes.byref(h), device.index, self.n, self.ld,
+                                     ctypes.c_void_p(stream))
+            _lib.check(rc, "otn_create")
+        self.h = h
+        self._stream = stream
+        info = (ctypes.c_int64 * 4)()
+        _lib.check(self.lib.otn_info(self.h, info), "otn_info")
+        self.coop_blocks = int(info[2])
+        self.workspace_bytes = int(info[3])
+
+    @classmethod
+    def get(cls, n, device):
+        key = (device.index, int(n))
+        ctx = cls._cache.get(key)
+        if ctx is None:
+            ctx = cls(n, device)
+            cls._cache[key] = ctx
+        ctx.sync_stream()
+        return ctx
+
+    def sync_stream(self):
+        s = torch().cuda.current_stream(self.device).cuda_stream
+        if s != self._stream:
+            _lib.check(self.lib.otn_set_stream(self.h, ctypes.c_void_p(s)), "otn_set_stream")
+            self._stream = s
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.otn_destroy(self.h)
+        except Exception:
+            pass
+
+    # ---- buffers ---------------------------------------------------------
+    def vec(self, init=None):
+        """Padded device vector (ld entries, zeros beyond n); returns the buffer."""
+        t = torch()
+        buf = t.zeros(self.ld, dtype=t.float64, device=self.device)
+        if init is not None:
+            self.upload(buf, init)
+        return buf
+
+    def upload(self, buf, values):
+        t = torch()
+        if is_tensor(values):
+            buf[: self.n].copy_(values.reshape(-1)[: self.n].to(dtype=t.float64), non_blocking=True)
+        else:
+            arr = np.ascontiguousarray(np.broadcast_to(np.asarray(values, dtype=np.float64),
+                                                       (self.n,)))
+            buf[: self.n].copy_(t.from_numpy(arr), non_blocking=False)
+        return buf
+
+    def download(self, buf):
+        return buf[: self.n].detach().cpu().numpy().copy()
+
+    def mat(self):
+        t = torch()
+        return t.zeros((self.n, self.ld), dtype=t.float64, device=self.device)
+
+    # ---- thin call helpers -----------------------------------------------
+    def call(self, name, *args):
+        rc = getattr(self.lib, name)(self.h, *args)
+        return _lib.check(rc, name)
+
+
+class DeviceCost:
+    """Device-resident cost matrix with leading dimension ld (multiple of 32)."""
+
+    def __init__(self, problem, device):
+        t = torch()
+        self.n = problem.n
+        self.ctx = Context.get(self.n, device)
+        ld = self.ctx.ld
+        C = problem.C
+        if is_tensor(C):
+            if not C.is_cuda:
+                C = C.to(device)
+            if ld == self.n and C.is_contiguous():
+                self.C = C
+            else:
+                self.C = t.zeros((self.n, ld), dtype=t.float64, device=device)
+                self.C[:, : self.n].copy_(C)
+        else:
+            host = t.from_numpy(np.ascontiguousarray(C, dtype=np.float64))
+            if ld == self.n:
+                self.C = host.to(device, non_blocking=False)
+            else:
+                self.C = t.zeros((self.n, ld), dtype=t.float64, device=device)
+                self.C[:, : self.n].copy_(host)
+        self._symmetric = None
+
+    @property
+    def symmetric(self):
+        """(C == C.T).all(), evaluated once (dual.py:80-88)."""
+        if self._symmetric is None:
+            sq = self.C[:, : self.n]
+            self._symmetric = bool(torch().equal(sq, sq.t()))
+        return self._symmetric
+
+    def ptr(self):
+        return vptr(self.C)

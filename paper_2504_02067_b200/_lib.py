@@ -1,0 +1,153 @@
+"""ctypes binding of the in-tree C-ABI library ``libotn_b200.so``.
+
+The library is the only compute path: there is no CPU fallback.  If it is
+missing or cannot be loaded, every solver entry point raises ``DeviceError``.
+The signatures below are exactly those declared in ``include/otn_b200.h``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import (
+    ConditioningError,
+    DeviceError,
+    DomainError,
+    NonconvergenceError,
+    PlanOverflowError,
+    StagnationError,
+)
+
+LIB_NAME = "libotn_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+OTN_OK = 0
+OTN_ERR_CUDA = 1
+OTN_ERR_ARG = 2
+OTN_ST_PLAN_OVERFLOW = 10
+OTN_ST_NONPOSITIVE_SUMS = 11
+OTN_ST_BREAKDOWN = 12
+OTN_ST_PRECOND = 13
+OTN_ST_NONCONVERGENCE = 14
+OTN_ST_STAGNATION = 15
+OTN_ST_DOMAIN = 16
+
+VEC_ADD_SUB, VEC_AXPY, VEC_STEP_V, VEC_EXTRAP, VEC_EXP, VEC_GRAD = range(6)
+RED_ROW_STATS, RED_GRAD_L1, RED_SUM_EXP, RED_DOT, RED_L1 = range(5)
+
+
+class SolveResult(ctypes.Structure):
+    _fields_ = [
+        ("status", ctypes.c_int32),
+        ("pcg_calls", ctypes.c_int32),
+        ("cg_iters", ctypes.c_int64),
+        ("hvps", ctypes.c_int64),
+        ("rho_final", ctypes.c_double),
+        ("resid_l1", ctypes.c_double),
+        ("slope", ctypes.c_double),
+        ("diag_rho", ctypes.c_double),
+        ("diag_resid", ctypes.c_double),
+    ]
+
+
+_P = ctypes.c_void_p
+_D = ctypes.c_double
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+_DP = ctypes.POINTER(ctypes.c_double)
+_IP = ctypes.POINTER(ctypes.c_int)
+
+# name -> argtypes (restype is int unless noted)
+SIGNATURES = {
+    "otn_abi_version": [],
+    "otn_last_error": [],
+    "otn_create": [ctypes.POINTER(_P), _I, _I64, _I64, _P],
+    "otn_destroy": [_P],
+    "otn_set_stream": [_P, _P],
+    "otn_info": [_P, ctypes.POINTER(_I64)],
+    "otn_read_flags": [_P, _IP],
+    "otn_lse_rows": [_P, _P, _D, _P, _P, _P],
+    "otn_lse_cols": [_P, _P, _I, _D, _P, _P, _P],
+    "otn_rebalance_cols": [_P, _P, _I, _D, _P, _P, _P],
+    "otn_trial_cols": [_P, _P, _I, _D, _P, _P, _P, _P, _D, _P, _DP],
+    "otn_materialize": [_P, _P, _D, _P, _P, _P, _P, _P, _P, _IP],
+    "otn_system_prep": [_P, _P, _P, _P, _P, _P, _IP],
+    "otn_square_matvec": [_P, _P, _P, _P],
+    "otn_matvec": [_P, _P, _P, _P],
+    "otn_rmatvec": [_P, _P, _P, _P],
+    "otn_apply_F": [_P, _P, _P, _P, _D, _P, _P],
+    "otn_apply_pc": [_P, _P, _P, _P, _P],
+    "otn_pcg": [_P, _P, _P, _P, _P, _D, _P, _D, _P, _I, _I64, ctypes.POINTER(SolveResult)],
+    "otn_newton": [_P, _P, _P, _P, _P, _P, _D, _D, _I, _I64, _P, _P,
+                   ctypes.POINTER(SolveResult)],
+    "otn_vec": [_P, _I, _D, _P, _P, _P, _P, _P],
+    "otn_reduce": [_P, _I, _P, _P, _P, _P, _DP, _IP],
+    "otn_round_plan": [_P, _P, _P, _P, _P, _DP, _IP],
+}
+
+_lib = None
+_load_error = None
+
+
+def load():
+    """Load (once) and return the ctypes library; raise DeviceError if absent."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    if _load_error is not None:
+        raise DeviceError(_load_error)
+    if not os.path.exists(LIB_PATH):
+        _load_error = (f"{LIB_PATH} not found: build it with `make -C "
+                       f"paper_2504_02067_b200/csrc` (or __graft_entry__.build()); "
+                       "there is no CPU fallback")
+        raise DeviceError(_load_error)
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:
+        _load_error = f"cannot load {LIB_PATH}: {exc}"
+        raise DeviceError(_load_error) from exc
+    for name, argtypes in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = ctypes.c_char_p if name == "otn_last_error" else ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    return list(SIGNATURES)
+
+
+def last_error():
+    return load().otn_last_error().decode(errors="replace")
+
+
+def check(rc, what):
+    """Map a non-solver return code onto DeviceError; pass solver codes through."""
+    if rc in (OTN_ERR_CUDA, OTN_ERR_ARG):
+        raise DeviceError(f"{what}: {last_error()}")
+    return rc
+
+
+def raise_for_status(rc, what, best=None, diagnostics=None, message=None):
+    """Raise the reference's exception class for a solver status code."""
+    if rc == OTN_OK:
+        return
+    check(rc, what)
+    if rc == OTN_ST_PLAN_OVERFLOW:
+        raise PlanOverflowError(message or "log-plan entry would overflow exp(); warm start is broken")
+    if rc == OTN_ST_NONPOSITIVE_SUMS:
+        raise ConditioningError("plan row/column sums must be strictly positive")
+    if rc == OTN_ST_PRECOND:
+        raise ConditioningError("preconditioner has a nonpositive diagonal entry")
+    if rc == OTN_ST_BREAKDOWN:
+        raise ConditioningError(message or "CG breakdown: nonpositive curvature along search direction")
+    if rc == OTN_ST_NONCONVERGENCE:
+        raise NonconvergenceError(message or "CG did not reach its tolerance", best=best,
+                                  diagnostics=diagnostics)
+    if rc == OTN_ST_STAGNATION:
+        raise StagnationError(message or "discount annealing stagnated")
+    if rc == OTN_ST_DOMAIN:
+        raise DomainError(message or "domain error")
+    raise DeviceError(f"{what}: unknown status {rc}")

@@ -1,0 +1,400 @@
+// extern "C" boundary: context management and the entry points declared in
+// include/otn_b200.h.  Every function validates its arguments, launches on the
+// context's stream, and returns an otn_status code.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "otn_internal.h"
+
+namespace otn {
+int coop_occupancy(int* blocks_per_sm);
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* what, cudaError_t e = cudaSuccess) {
+  char buf[512];
+  if (e != cudaSuccess)
+    snprintf(buf, sizeof(buf), "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+  else
+    snprintf(buf, sizeof(buf), "%s", what);
+  g_err = buf;
+  return code;
+}
+
+#define OTN_CUDA(call, what)                               \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) return fail(OTN_ERR_CUDA, what, e_); \
+  } while (0)
+
+#define OTN_REQUIRE(cond, what) \
+  do {                          \
+    if (!(cond)) return fail(OTN_ERR_ARG, what); \
+  } while (0)
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+int sync_copy(otn_ctx* x, void* host, const void* dev, size_t bytes, const char* what) {
+  OTN_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, x->stream), what);
+  OTN_CUDA(cudaStreamSynchronize(x->stream), what);
+  return OTN_OK;
+}
+
+otn::CoopArgs base_args(otn_ctx* x, const double* P) {
+  otn::CoopArgs a{};
+  a.P = P;
+  a.n = x->n;
+  a.ld = x->ld;
+  a.r = x->r;
+  a.z = x->z;
+  a.p = x->p;
+  a.q = x->q;
+  a.M = x->M;
+  a.wc = x->wc;
+  a.sv = x->sv;
+  a.wpart = x->wpart;
+  a.red = x->red;
+  a.res = x->dres;
+  return a;
+}
+
+int finish_solve(otn_ctx* x, otn_solve_result* host_res, const char* what) {
+  int rc = sync_copy(x, x->h_res, x->dres, sizeof(otn::DevResult), what);
+  if (rc) return rc;
+  if (host_res) std::memcpy(host_res, x->h_res, sizeof(otn_solve_result));
+  return x->h_res->status;
+}
+
+}  // namespace
+
+static_assert(sizeof(otn_solve_result) == sizeof(otn::DevResult), "result layout");
+
+extern "C" {
+
+int otn_abi_version(void) { return OTN_ABI_VERSION; }
+
+const char* otn_last_error(void) { return g_err.c_str(); }
+
+int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
+  OTN_REQUIRE(out != nullptr, "otn_create: out is NULL");
+  OTN_REQUIRE(n >= 1, "otn_create: n must be >= 1");
+  OTN_REQUIRE(ld >= n && ld % 32 == 0, "otn_create: ld must be >= n and a multiple of 32");
+  *out = nullptr;
+  OTN_CUDA(cudaSetDevice(device), "otn_create: cudaSetDevice");
+  otn_ctx* x = new otn_ctx();
+  std::memset(x, 0, sizeof(otn_ctx));
+  x->device = device;
+  x->n = n;
+  x->ld = ld;
+  x->stream = static_cast<cudaStream_t>(stream);
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) { delete x; return fail(OTN_ERR_CUDA, "otn_create: properties", e); }
+  if (!prop.cooperativeLaunch) { delete x; return fail(OTN_ERR_CUDA, "otn_create: no cooperative launch"); }
+  x->num_sms = prop.multiProcessorCount;
+  int per_sm = 0;
+  e = (cudaError_t)otn::coop_occupancy(&per_sm);
+  if (e != cudaSuccess || per_sm < 1) {
+    delete x;
+    return fail(OTN_ERR_CUDA, "otn_create: persistent solver does not fit on an SM", e);
+  }
+  x->coop_blocks = x->num_sms;   // one CTA per SM (co-residency guaranteed)
+  // column-reduction slabs: ~4 CTAs per SM over ld/64 column tiles
+  {
+    const int64_t tiles = (ld + otn::kColTile - 1) / otn::kColTile;
+    int64_t want = (4LL * x->num_sms + tiles - 1) / tiles;
+    if (want < 1) want = 1;
+    if (want > 64) want = 64;
+    if (want > n) want = n;
+    x->lse_slabs = int(want);
+  }
+  const size_t vec = align_up(size_t(ld) * sizeof(double), 256);
+  size_t off = 0;
+  size_t o_r = off; off += vec;
+  size_t o_z = off; off += vec;
+  size_t o_p = off; off += vec;
+  size_t o_q = off; off += vec;
+  size_t o_M = off; off += vec;
+  size_t o_wc = off; off += vec;
+  size_t o_sv = off; off += vec;
+  size_t o_t0 = off; off += vec;
+  size_t o_t1 = off; off += vec;
+  size_t o_wp = off; off += align_up(size_t(x->coop_blocks) * ld * sizeof(double), 256);
+  size_t o_red = off; off += align_up(size_t(otn::kRedSlots) * x->coop_blocks * otn::kRedWidth * sizeof(double), 256);
+  size_t o_lse = off; off += align_up(size_t(x->lse_slabs) * ld * 2 * sizeof(double), 256);
+  size_t o_sc = off; off += align_up(64 * sizeof(double), 256);
+  size_t o_fl = off; off += align_up(16 * sizeof(int), 256);
+  size_t o_res = off; off += align_up(sizeof(otn::DevResult), 256);
+  x->ws_bytes = off;
+  e = cudaMalloc(&x->ws, off);
+  if (e != cudaSuccess) { delete x; return fail(OTN_ERR_CUDA, "otn_create: cudaMalloc", e); }
+  cudaMemset(x->ws, 0, off);
+  char* base = static_cast<char*>(x->ws);
+  x->r = (double*)(base + o_r);
+  x->z = (double*)(base + o_z);
+  x->p = (double*)(base + o_p);
+  x->q = (double*)(base + o_q);
+  x->M = (double*)(base + o_M);
+  x->wc = (double*)(base + o_wc);
+  x->sv = (double*)(base + o_sv);
+  x->vtmp0 = (double*)(base + o_t0);
+  x->vtmp1 = (double*)(base + o_t1);
+  x->wpart = (double*)(base + o_wp);
+  x->red = (double*)(base + o_red);
+  x->lse_part = (double*)(base + o_lse);
+  x->scal = (double*)(base + o_sc);
+  x->flags = (int*)(base + o_fl);
+  x->dres = (otn::DevResult*)(base + o_res);
+  e = cudaMallocHost((void**)&x->h_scal, 64 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMallocHost((void**)&x->h_flags, 16 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMallocHost((void**)&x->h_res, sizeof(otn::DevResult));
+  if (e != cudaSuccess) { otn_destroy(x); return fail(OTN_ERR_CUDA, "otn_create: pinned host", e); }
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { otn_destroy(x); return fail(OTN_ERR_CUDA, "otn_create: sync", e); }
+  *out = x;
+  return OTN_OK;
+}
+
+int otn_destroy(otn_ctx* x) {
+  if (!x) return OTN_OK;
+  if (x->ws) cudaFree(x->ws);
+  if (x->h_scal) cudaFreeHost(x->h_scal);
+  if (x->h_flags) cudaFreeHost(x->h_flags);
+  if (x->h_res) cudaFreeHost(x->h_res);
+  delete x;
+  return OTN_OK;
+}
+
+int otn_set_stream(otn_ctx* x, void* stream) {
+  OTN_REQUIRE(x, "otn_set_stream: NULL ctx");
+  x->stream = static_cast<cudaStream_t>(stream);
+  return OTN_OK;
+}
+
+int otn_info(const otn_ctx* x, int64_t* out4) {
+  OTN_REQUIRE(x && out4, "otn_info: NULL argument");
+  out4[0] = x->n;
+  out4[1] = x->ld;
+  out4[2] = x->coop_blocks;
+  out4[3] = int64_t(x->ws_bytes);
+  return OTN_OK;
+}
+
+int otn_read_flags(otn_ctx* x, int* host4) {
+  OTN_REQUIRE(x && host4, "otn_read_flags: NULL argument");
+  int rc = sync_copy(x, x->h_flags, x->flags, 4 * sizeof(int), "otn_read_flags");
+  if (rc) return rc;
+  std::memcpy(host4, x->h_flags, 4 * sizeof(int));
+  return OTN_OK;
+}
+
+// ---- log-domain reductions -----------------------------------------------
+int otn_lse_rows(otn_ctx* x, const double* C, double ng, const double* outer, const double* inner,
+                 double* out) {
+  OTN_REQUIRE(x && C && inner && out, "otn_lse_rows: NULL argument");
+  OTN_CUDA(otn::launch_lse_rows(x, C, ng, outer, nullptr, inner, nullptr, 0.0, 0, out),
+           "otn_lse_rows");
+  return OTN_OK;
+}
+
+static int lse_cols_any(otn_ctx* x, const double* C, int sym, double ng, const double* outer,
+                        const double* outer_d, const double* inner, const double* inner_d,
+                        double alpha, int mode, double* out, const char* what) {
+  cudaError_t e = sym ? otn::launch_lse_rows(x, C, ng, outer, outer_d, inner, inner_d, alpha, mode, out)
+                      : otn::launch_lse_cols(x, C, ng, outer, outer_d, inner, inner_d, alpha, mode, out);
+  OTN_CUDA(e, what);
+  return OTN_OK;
+}
+
+int otn_lse_cols(otn_ctx* x, const double* C, int sym, double ng, const double* outer,
+                 const double* inner, double* out) {
+  OTN_REQUIRE(x && C && inner && out, "otn_lse_cols: NULL argument");
+  return lse_cols_any(x, C, sym, ng, outer, nullptr, inner, nullptr, 0.0, 0, out, "otn_lse_cols");
+}
+
+int otn_rebalance_cols(otn_ctx* x, const double* C, int sym, double ng, const double* log_c,
+                       const double* u, double* v_out) {
+  OTN_REQUIRE(x && C && log_c && u && v_out, "otn_rebalance_cols: NULL argument");
+  return lse_cols_any(x, C, sym, ng, log_c, nullptr, u, nullptr, 0.0, 1, v_out,
+                      "otn_rebalance_cols");
+}
+
+int otn_trial_cols(otn_ctx* x, const double* C, int sym, double ng, const double* u,
+                   const double* du, const double* v, const double* dv, double alpha, double* out,
+                   double* host_mass) {
+  OTN_REQUIRE(x && C && u && du && v && dv && out, "otn_trial_cols: NULL argument");
+  int rc = lse_cols_any(x, C, sym, ng, v, dv, u, du, alpha, 0, out, "otn_trial_cols");
+  if (rc) return rc;
+  if (host_mass) {
+    OTN_CUDA(otn::launch_reduce(x, OTN_RED_SUM_EXP, x->n, out, nullptr, nullptr, nullptr, x->scal,
+                                x->flags + 4),
+             "otn_trial_cols: mass");
+    rc = sync_copy(x, x->h_scal, x->scal, sizeof(double), "otn_trial_cols: mass copy");
+    if (rc) return rc;
+    *host_mass = x->h_scal[0];
+  }
+  return OTN_OK;
+}
+
+// ---- plan ----------------------------------------------------------------
+int otn_materialize(otn_ctx* x, const double* C, double ng, const double* u, const double* v,
+                    double* P, const double* icP, const double* rP, double* mu, int* host_overflow) {
+  OTN_REQUIRE(x && C && u && v && P, "otn_materialize: NULL argument");
+  OTN_REQUIRE(!icP || (rP && mu), "otn_materialize: icP needs rP and mu");
+  OTN_CUDA(cudaMemsetAsync(x->flags + 0, 0, sizeof(int), x->stream), "otn_materialize: flag");
+  OTN_CUDA(otn::launch_materialize(x, C, ng, u, v, P, icP, rP, mu, x->flags + 0),
+           "otn_materialize");
+  if (host_overflow) {
+    int rc = sync_copy(x, x->h_flags, x->flags, sizeof(int), "otn_materialize: flag copy");
+    if (rc) return rc;
+    *host_overflow = x->h_flags[0];
+    if (x->h_flags[0]) return OTN_ST_PLAN_OVERFLOW;
+  }
+  return OTN_OK;
+}
+
+int otn_system_prep(otn_ctx* x, const double* lr, const double* lc, double* rP, double* cP,
+                    double* icP, int* host_bad) {
+  OTN_REQUIRE(x && lr && lc && rP && cP && icP, "otn_system_prep: NULL argument");
+  OTN_CUDA(cudaMemsetAsync(x->flags + 1, 0, sizeof(int), x->stream), "otn_system_prep: flag");
+  OTN_CUDA(otn::launch_sys_prep(x, lr, lc, rP, cP, icP, x->flags + 1), "otn_system_prep");
+  if (host_bad) {
+    int rc = sync_copy(x, x->h_flags, x->flags + 1, sizeof(int), "otn_system_prep: flag copy");
+    if (rc) return rc;
+    *host_bad = x->h_flags[0];
+    if (x->h_flags[0]) return OTN_ST_NONPOSITIVE_SUMS;
+  }
+  return OTN_OK;
+}
+
+int otn_square_matvec(otn_ctx* x, const double* P, const double* w, double* out) {
+  OTN_REQUIRE(x && P && w && out, "otn_square_matvec: NULL argument");
+  OTN_CUDA(otn::launch_square_matvec(x, P, w, out), "otn_square_matvec");
+  return OTN_OK;
+}
+
+// ---- HVP seam operators (single cooperative launch each) -------------------
+static int coop_op(otn_ctx* x, int mode, const double* P, const double* rP, const double* cP,
+                   double rho, const double* xin, double* out, const char* what) {
+  otn::CoopArgs a = base_args(x, P);
+  a.mode = mode;
+  a.rP = rP;
+  a.cP = cP;
+  a.rho = rho;
+  a.xin = xin;
+  a.d = out;
+  OTN_CUDA(otn::launch_coop(x, a), what);
+  return OTN_OK;
+}
+
+int otn_matvec(otn_ctx* x, const double* P, const double* v, double* out) {
+  OTN_REQUIRE(x && P && v && out, "otn_matvec: NULL argument");
+  return coop_op(x, otn::kModeMatvec, P, nullptr, nullptr, 0.0, v, out, "otn_matvec");
+}
+
+int otn_rmatvec(otn_ctx* x, const double* P, const double* v, double* out) {
+  OTN_REQUIRE(x && P && v && out, "otn_rmatvec: NULL argument");
+  return coop_op(x, otn::kModeRmatvec, P, nullptr, nullptr, 0.0, v, out, "otn_rmatvec");
+}
+
+int otn_apply_F(otn_ctx* x, const double* P, const double* rP, const double* cP, double rho,
+                const double* d, double* out) {
+  OTN_REQUIRE(x && P && rP && cP && d && out, "otn_apply_F: NULL argument");
+  return coop_op(x, otn::kModeHvp, P, rP, cP, rho, d, out, "otn_apply_F");
+}
+
+int otn_apply_pc(otn_ctx* x, const double* P, const double* cP, const double* d, double* out) {
+  OTN_REQUIRE(x && P && cP && d && out, "otn_apply_pc: NULL argument");
+  return coop_op(x, otn::kModePc, P, nullptr, cP, 0.0, d, out, "otn_apply_pc");
+}
+
+// ---- solvers ---------------------------------------------------------------
+int otn_pcg(otn_ctx* x, const double* P, const double* rP, const double* cP, const double* mu,
+            double rho, const double* b, double tol, double* xv, int has_x0, int64_t max_iters,
+            otn_solve_result* host_res) {
+  OTN_REQUIRE(x && P && rP && cP && mu && b && xv, "otn_pcg: NULL argument");
+  OTN_REQUIRE(max_iters >= 0, "otn_pcg: max_iters < 0");
+  otn::CoopArgs a = base_args(x, P);
+  a.mode = otn::kModePcg;
+  a.rP = rP;
+  a.cP = cP;
+  a.mu = mu;
+  a.rho = rho;
+  a.b = b;
+  a.tol = tol;
+  a.d = xv;
+  a.has_x0 = has_x0;
+  a.max_iters = max_iters;
+  OTN_CUDA(otn::launch_coop(x, a), "otn_pcg");
+  return finish_solve(x, host_res, "otn_pcg: result");
+}
+
+int otn_newton(otn_ctx* x, const double* P, const double* rP, const double* cP, const double* mu,
+               const double* g, double eta, double rho0, int zero_init, int64_t max_iters,
+               double* d_u, double* d_v, otn_solve_result* host_res) {
+  OTN_REQUIRE(x && P && rP && cP && mu && g && d_u, "otn_newton: NULL argument");
+  OTN_REQUIRE(max_iters >= 0, "otn_newton: max_iters < 0");
+  otn::CoopArgs a = base_args(x, P);
+  a.mode = otn::kModeNewton;
+  a.rP = rP;
+  a.cP = cP;
+  a.mu = mu;
+  a.g = g;
+  a.eta = eta;
+  a.rho0 = rho0;
+  a.zero_init = zero_init;
+  a.max_iters = max_iters;
+  a.d = d_u;
+  a.dv = d_v;
+  a.pre_flags = x->flags;
+  OTN_CUDA(otn::launch_coop(x, a), "otn_newton");
+  return finish_solve(x, host_res, "otn_newton: result");
+}
+
+// ---- vector work -----------------------------------------------------------
+int otn_vec(otn_ctx* x, int op, double s, const double* a, const double* b, const double* c,
+            const double* d, double* out) {
+  OTN_REQUIRE(x && a && out, "otn_vec: NULL argument");
+  OTN_REQUIRE(op >= OTN_VEC_ADD_SUB && op <= OTN_VEC_GRAD, "otn_vec: bad op");
+  OTN_CUDA(otn::launch_vec(x, op, x->n, s, a, b, c, d, out), "otn_vec");
+  return OTN_OK;
+}
+
+int otn_reduce(otn_ctx* x, int op, const double* a, const double* b, const double* c,
+               const double* d, double* host_out, int* host_flags) {
+  OTN_REQUIRE(x && a && host_out, "otn_reduce: NULL argument");
+  OTN_REQUIRE(op >= OTN_RED_ROW_STATS && op <= OTN_RED_L1, "otn_reduce: bad op");
+  OTN_CUDA(cudaMemsetAsync(x->flags + 2, 0, sizeof(int), x->stream), "otn_reduce: flag");
+  OTN_CUDA(otn::launch_reduce(x, op, x->n, a, b, c, d, x->scal + 8, x->flags + 2), "otn_reduce");
+  OTN_CUDA(cudaMemcpyAsync(x->h_scal + 8, x->scal + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                           x->stream), "otn_reduce: copy");
+  OTN_CUDA(cudaMemcpyAsync(x->h_flags + 2, x->flags + 2, sizeof(int), cudaMemcpyDeviceToHost,
+                           x->stream), "otn_reduce: copy");
+  OTN_CUDA(cudaStreamSynchronize(x->stream), "otn_reduce: sync");
+  host_out[0] = x->h_scal[8];
+  host_out[1] = x->h_scal[9];
+  if (host_flags) *host_flags = x->h_flags[2];
+  return OTN_OK;
+}
+
+int otn_round_plan(otn_ctx* x, double* P, const double* C, const double* r, const double* c,
+                   double* host_out, int* host_flags) {
+  OTN_REQUIRE(x && P && r && c && host_out, "otn_round_plan: NULL argument");
+  OTN_CUDA(cudaMemsetAsync(x->flags + 3, 0, sizeof(int), x->stream), "otn_round_plan: flag");
+  OTN_CUDA(otn::launch_round(x, P, C, r, c, x->scal + 16, x->flags + 3), "otn_round_plan");
+  OTN_CUDA(cudaMemcpyAsync(x->h_scal + 16, x->scal + 16, 4 * sizeof(double),
+                           cudaMemcpyDeviceToHost, x->stream), "otn_round_plan: copy");
+  OTN_CUDA(cudaMemcpyAsync(x->h_flags + 3, x->flags + 3, sizeof(int), cudaMemcpyDeviceToHost,
+                           x->stream), "otn_round_plan: copy");
+  OTN_CUDA(cudaStreamSynchronize(x->stream), "otn_round_plan: sync");
+  host_out[0] = x->h_scal[16 + 3];   // primal <P, C>
+  host_out[1] = x->h_scal[16 + 2];   // deficit
+  if (host_flags) *host_flags = x->h_flags[3];
+  return OTN_OK;
+}
+
+}  // extern "C"

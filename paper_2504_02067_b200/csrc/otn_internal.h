@@ -1,0 +1,101 @@
+// Internal declarations shared by the kernel translation units and the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/otn_b200.h"
+
+namespace otn {
+
+constexpr int kCoopThreads = 512;       // one CTA per SM for the persistent solver
+constexpr int kLseThreads = 256;        // 8 warps: one row per warp
+constexpr int kColTile = 64;            // columns per CTA in column reductions
+constexpr int kRedSlots = 2;            // rotating grid-reduction slots
+constexpr int kRedWidth = 4;            // doubles per CTA per slot
+
+// Device-side solver record (mirrored by otn_solve_result on the host).
+struct DevResult {
+  int32_t status;
+  int32_t pcg_calls;    // pcg_solve invocations (diag_prc is tallied on the first)
+  int64_t cg_iters;     // newton: total CG iterations; pcg: iterations
+  int64_t hvps;         // Hessian-vector products with rho != 0 (2 matvec passes each)
+  double rho_final;     // rho of the last PCG call (newton.py:209)
+  double resid_l1;      // undiscounted residual (newton) / recurrence residual (pcg)
+  double slope;         // -(grad_u . d_u)  (projector.py:205)
+  double diag_rho;      // NonconvergenceError diagnostics (newton.py:168-172)
+  double diag_resid;
+};
+
+}  // namespace otn
+
+struct otn_ctx {
+  int device;
+  int64_t n, ld;
+  cudaStream_t stream;
+  int num_sms;
+  int coop_blocks;        // grid size of the persistent solver (all co-resident)
+  int lse_slabs;          // row slabs of the column reductions
+  // device workspace (one allocation)
+  void* ws;
+  size_t ws_bytes;
+  double *r, *z, *p, *q, *M, *wc, *sv, *vtmp0, *vtmp1;   // length ld each
+  double* wpart;          // coop_blocks x ld column partials
+  double* red;            // kRedSlots x coop_blocks x kRedWidth grid-reduction partials
+  double* lse_part;       // lse_slabs x ld x 2 (m, s) column-LSE partials
+  double* scal;           // 64 device scalars
+  int* flags;             // 16 device flag words
+  otn::DevResult* dres;
+  // pinned host mirrors
+  double* h_scal;
+  int* h_flags;
+  otn::DevResult* h_res;
+};
+
+// Launchers (all stream-ordered on ctx->stream; return cudaError_t).
+namespace otn {
+cudaError_t launch_lse_rows(otn_ctx* x, const double* C, double ng, const double* outer,
+                            const double* outer_d, const double* inner, const double* inner_d,
+                            double alpha, int mode, double* out);
+cudaError_t launch_lse_cols(otn_ctx* x, const double* C, double ng, const double* outer,
+                            const double* outer_d, const double* inner, const double* inner_d,
+                            double alpha, int mode, double* out);
+cudaError_t launch_materialize(otn_ctx* x, const double* C, double ng, const double* u,
+                               const double* v, double* P, const double* icP, const double* rP,
+                               double* mu, int* flag);
+cudaError_t launch_sys_prep(otn_ctx* x, const double* log_rP, const double* log_cP, double* rP,
+                            double* cP, double* icP, int* flag);
+cudaError_t launch_square_matvec(otn_ctx* x, const double* P, const double* w, double* out);
+
+// Persistent cooperative solver.
+enum CoopMode { kModeNewton = 0, kModePcg = 1, kModeHvp = 2, kModePc = 3, kModeMatvec = 4,
+                kModeRmatvec = 5 };
+struct CoopArgs {
+  const double* P;
+  int64_t n, ld;
+  const double* rP;
+  const double* cP;
+  const double* mu;
+  const double* g;        // newton: grad_u
+  const double* b;        // pcg: right-hand side
+  const double* xin;      // hvp / pc / matvec: input vector
+  double* d;              // newton: d_u out; pcg: x in/out; others: output vector
+  double* dv;             // newton: optional d_v out
+  double eta, rho0, rho, tol;
+  int zero_init, has_x0, mode, pad;
+  int64_t max_iters;
+  const int* pre_flags;   // materialize / prep flags checked first (nullable)
+  // workspace
+  double *r, *z, *p, *q, *M, *wc, *sv, *wpart, *red;
+  DevResult* res;
+};
+cudaError_t launch_coop(otn_ctx* x, const CoopArgs& a);
+
+// Vector kernels and single-CTA reductions.
+cudaError_t launch_vec(otn_ctx* x, int op, int64_t n, double s0, const double* a, const double* b,
+                       const double* c, const double* d, double* out);
+cudaError_t launch_reduce(otn_ctx* x, int op, int64_t n, const double* a, const double* b,
+                          const double* c, const double* d, double* dst, int* flag);
+cudaError_t launch_round(otn_ctx* x, double* P, const double* C, const double* r, const double* c,
+                         double* scratch_scalars, int* flag);
+}  // namespace otn

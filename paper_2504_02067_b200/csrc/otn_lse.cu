@@ -1,0 +1,274 @@
+// Log-domain reductions over the stored cost (K1/K2/K3), plan materialization
+// with the fused Jacobi diagonal (K4+K5), and the system prep vectors.
+//
+// All of these stream the n x n cost (or plan) once from HBM with 128-bit
+// non-allocating loads and do their math in FP64 registers; they are HBM /
+// FP64-pipe bound (exp costs ~20 FP64 instructions per entry).
+#include "otn_common.cuh"
+#include "otn_internal.h"
+
+namespace otn {
+
+struct LseArgs {
+  const double* C;
+  int64_t n, ld;
+  double ng;                // -gamma
+  const double* outer;      // nullable -> 0.0
+  const double* outer_d;    // nullable; outer_eff = outer + alpha*outer_d
+  const double* inner;
+  const double* inner_d;    // nullable; inner_eff = inner + alpha*inner_d
+  double alpha;
+  int mode;                 // 0: out = outer + lse;  1: out = outer - lse
+  double* out;
+};
+
+__device__ __forceinline__ double eff(const double* base, const double* dir, double alpha,
+                                      int64_t j) {
+  double b = __ldg(base + j);
+  // numpy: base + alpha*dir, each operation rounded (dual.py:174-175)
+  return dir ? __dadd_rn(b, __dmul_rn(alpha, __ldg(dir + j))) : b;
+}
+
+__device__ __forceinline__ double finish(const LseArgs& a, int64_t j, double lse) {
+  double o = a.outer ? eff(a.outer, a.outer_d, a.alpha, j) : 0.0;
+  return a.mode == 0 ? __dadd_rn(o, lse) : __dsub_rn(o, lse);
+}
+
+// ---------------------------------------------------------------------------
+// Row LSE: one warp per row; each lane streams 8 entries (four 16-byte loads)
+// per step, keeps an online (max, sum-exp) pair and rescales at most once per
+// step, so the cost is ~1.1 exp per entry.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kLseThreads) k_lse_rows(LseArgs a) {
+  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= a.n) return;
+  const double* crow = a.C + row * a.ld;
+  const int64_t n = a.n;
+  double m = OTN_NINF, s = 0.0;
+  for (int64_t base = 0; base < n; base += 256) {
+    double b[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t j = base + 64 * k + 2 * lane;
+      if (j < n) {
+        const double2 c = ld_stream2(crow + j);
+        b[2 * k] = __dadd_rn(__dmul_rn(a.ng, c.x), eff(a.inner, a.inner_d, a.alpha, j));
+        b[2 * k + 1] = (j + 1 < n)
+            ? __dadd_rn(__dmul_rn(a.ng, c.y), eff(a.inner, a.inner_d, a.alpha, j + 1))
+            : OTN_NINF;
+      } else {
+        b[2 * k] = OTN_NINF;
+        b[2 * k + 1] = OTN_NINF;
+      }
+    }
+    double cm = b[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) cm = fmax(cm, b[k]);
+    if (cm > m) {
+      s = s * exp(m - cm);
+      m = cm;
+    }
+    if (m != OTN_NINF) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += exp(b[k] - m);
+    }
+  }
+  warp_lse(m, s);
+  if (lane == 0) a.out[row] = finish(a, row, lse_value(m, s));
+}
+
+// ---------------------------------------------------------------------------
+// Column LSE (asymmetric C): CTA = 64 columns x one slab of rows; each warp
+// walks rows 4 at a time (coalesced 512-byte row segments), lanes own 2
+// columns.  Partial (max, sum) per slab go to the workspace and a finalize
+// kernel merges the slabs in fixed order.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kLseThreads) k_lse_cols_part(LseArgs a, int64_t slab_rows,
+                                                               double* part) {
+  __shared__ double sm_m[8][kColTile];
+  __shared__ double sm_s[8][kColTile];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j = int64_t(blockIdx.x) * kColTile + 2 * lane;
+  const int64_t i0 = int64_t(blockIdx.y) * slab_rows;
+  const int64_t i1 = min(a.n, i0 + slab_rows);
+  const bool c0 = j < a.n, c1 = j + 1 < a.n;
+  double m0 = OTN_NINF, s0 = 0.0, m1 = OTN_NINF, s1 = 0.0;
+  for (int64_t i = i0 + 4 * warp; i < i1; i += 32) {
+    double b0[4], b1[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t ii = i + k;
+      if (ii < i1 && c0) {
+        const double2 c = ld_stream2(a.C + ii * a.ld + j);
+        const double in = eff(a.inner, a.inner_d, a.alpha, ii);
+        b0[k] = __dadd_rn(__dmul_rn(a.ng, c.x), in);
+        b1[k] = c1 ? __dadd_rn(__dmul_rn(a.ng, c.y), in) : OTN_NINF;
+      } else {
+        b0[k] = OTN_NINF;
+        b1[k] = OTN_NINF;
+      }
+    }
+    double cm0 = fmax(fmax(b0[0], b0[1]), fmax(b0[2], b0[3]));
+    double cm1 = fmax(fmax(b1[0], b1[1]), fmax(b1[2], b1[3]));
+    if (cm0 > m0) { s0 = s0 * exp(m0 - cm0); m0 = cm0; }
+    if (cm1 > m1) { s1 = s1 * exp(m1 - cm1); m1 = cm1; }
+    if (m0 != OTN_NINF) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s0 += exp(b0[k] - m0);
+    }
+    if (m1 != OTN_NINF) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s1 += exp(b1[k] - m1);
+    }
+  }
+  sm_m[warp][2 * lane] = m0;
+  sm_s[warp][2 * lane] = s0;
+  sm_m[warp][2 * lane + 1] = m1;
+  sm_s[warp][2 * lane + 1] = s1;
+  __syncthreads();
+  if (threadIdx.x < kColTile) {
+    const int t = threadIdx.x;
+    double m = sm_m[0][t], s = sm_s[0][t];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) lse_merge(m, s, sm_m[w][t], sm_s[w][t]);
+    const int64_t jj = int64_t(blockIdx.x) * kColTile + t;
+    if (jj < a.ld) {
+      double* dst = part + (int64_t(blockIdx.y) * a.ld + jj) * 2;
+      dst[0] = m;
+      dst[1] = s;
+    }
+  }
+}
+
+__global__ void k_lse_cols_fin(LseArgs a, int slabs, const double* part) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= a.n) return;
+  double m = OTN_NINF, s = 0.0;
+  for (int k = 0; k < slabs; ++k) {
+    const double* src = part + (int64_t(k) * a.ld + j) * 2;
+    lse_merge(m, s, src[0], src[1]);
+  }
+  a.out[j] = finish(a, j, lse_value(m, s));
+}
+
+// ---------------------------------------------------------------------------
+// Plan: P_ij = exp((ng*C_ij + v_j) + u_i), one warp per row, 16-byte stores,
+// zeros in the padding columns.  Fused K5: mu_i = (sum_j P_ij^2 icP_j)/rP_i.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kLseThreads) k_materialize(const double* __restrict__ C,
+    int64_t n, int64_t ld, double ng, const double* __restrict__ u, const double* __restrict__ v,
+    double* __restrict__ P, const double* __restrict__ icP, const double* __restrict__ rP,
+    double* __restrict__ mu, int* __restrict__ flag) {
+  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double* crow = C + row * ld;
+  double* prow = P + row * ld;
+  const double ui = __ldg(u + row);
+  double acc = 0.0, mx = OTN_NINF;
+  for (int64_t base = 0; base < ld; base += 256) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t j = base + 64 * k + 2 * lane;
+      if (j < ld) {
+        double e0 = OTN_NINF, e1 = OTN_NINF;
+        if (j < n) {
+          const double2 c = ld_stream2(crow + j);
+          e0 = __dadd_rn(__dadd_rn(__dmul_rn(ng, c.x), __ldg(v + j)), ui);
+          if (j + 1 < n) e1 = __dadd_rn(__dadd_rn(__dmul_rn(ng, c.y), __ldg(v + j + 1)), ui);
+        }
+        mx = fmax(mx, fmax(e0, e1));
+        const double p0 = exp(e0), p1 = exp(e1);
+        *reinterpret_cast<double2*>(prow + j) = make_double2(p0, p1);
+        if (icP) {
+          if (j < n) acc = fma(__dmul_rn(p0, p0), __ldg(icP + j), acc);
+          if (j + 1 < n) acc = fma(__dmul_rn(p1, p1), __ldg(icP + j + 1), acc);
+        }
+      }
+    }
+  }
+  mx = warp_max(mx);
+  if (icP) acc = warp_sum(acc);
+  if (lane == 0) {
+    if (mx > 700.0) atomicOr(flag, 1);          // _kernels.py:53-58
+    if (icP) mu[row] = __ddiv_rn(acc, __ldg(rP + row));
+  }
+}
+
+__global__ void k_sys_prep(int64_t n, const double* __restrict__ lr, const double* __restrict__ lc,
+                           double* rP, double* cP, double* icP, int* flag) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double rp = exp(lr[i]), cp = exp(lc[i]);
+  rP[i] = rp;
+  cP[i] = cp;
+  icP[i] = __ddiv_rn(1.0, cp);                  // newton.py:111: 1.0 / self.cP
+  if (rp <= 0.0 || cp <= 0.0) atomicOr(flag, 2);  // newton.py:76-77
+}
+
+// (P*P) @ w — standalone seam operator (_kernels.py:64-74); the solver uses
+// the copy fused into k_materialize.
+__global__ void __launch_bounds__(kLseThreads) k_square_matvec(const double* __restrict__ P,
+    int64_t n, int64_t ld, const double* __restrict__ w, double* __restrict__ out) {
+  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double* prow = P + row * ld;
+  double acc = 0.0;
+  for (int64_t j = 2 * lane; j < n; j += 64) {
+    const double2 p = ld_stream2(prow + j);
+    acc = fma(__dmul_rn(p.x, p.x), __ldg(w + j), acc);
+    if (j + 1 < n) acc = fma(__dmul_rn(p.y, p.y), __ldg(w + j + 1), acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) out[row] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static inline unsigned rows_grid(int64_t n) {
+  return unsigned((n + (kLseThreads / 32) - 1) / (kLseThreads / 32));
+}
+
+cudaError_t launch_lse_rows(otn_ctx* x, const double* C, double ng, const double* outer,
+                            const double* outer_d, const double* inner, const double* inner_d,
+                            double alpha, int mode, double* out) {
+  LseArgs a{C, x->n, x->ld, ng, outer, outer_d, inner, inner_d, alpha, mode, out};
+  k_lse_rows<<<rows_grid(x->n), kLseThreads, 0, x->stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lse_cols(otn_ctx* x, const double* C, double ng, const double* outer,
+                            const double* outer_d, const double* inner, const double* inner_d,
+                            double alpha, int mode, double* out) {
+  LseArgs a{C, x->n, x->ld, ng, outer, outer_d, inner, inner_d, alpha, mode, out};
+  const int slabs = x->lse_slabs;
+  const int64_t slab_rows = (x->n + slabs - 1) / slabs;
+  dim3 grid(unsigned((x->ld + kColTile - 1) / kColTile), unsigned(slabs));
+  k_lse_cols_part<<<grid, kLseThreads, 0, x->stream>>>(a, slab_rows, x->lse_part);
+  k_lse_cols_fin<<<unsigned((x->n + 255) / 256), 256, 0, x->stream>>>(a, slabs, x->lse_part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_materialize(otn_ctx* x, const double* C, double ng, const double* u,
+                               const double* v, double* P, const double* icP, const double* rP,
+                               double* mu, int* flag) {
+  k_materialize<<<rows_grid(x->n), kLseThreads, 0, x->stream>>>(C, x->n, x->ld, ng, u, v, P, icP,
+                                                                 rP, mu, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sys_prep(otn_ctx* x, const double* lr, const double* lc, double* rP,
+                            double* cP, double* icP, int* flag) {
+  k_sys_prep<<<unsigned((x->n + 255) / 256), 256, 0, x->stream>>>(x->n, lr, lc, rP, cP, icP, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_square_matvec(otn_ctx* x, const double* P, const double* w, double* out) {
+  k_square_matvec<<<rows_grid(x->n), kLseThreads, 0, x->stream>>>(P, x->n, x->ld, w, out);
+  return cudaGetLastError();
+}
+
+}  // namespace otn

@@ -1,0 +1,355 @@
+"""Dual potentials and the log-domain plan, resident in HBM (mirrors ``dual.py:22-219``).
+
+The plan implied by potentials (u, v) at inverse temperature gamma is
+``P_ij = exp(u_i + v_j - gamma*C_ij)``.  Row and column sums are always
+log-domain reductions over the stored cost (kernels K1/K2 of the C-ABI), never
+sums of the linear plan, and are cached until u, v or gamma is reassigned —
+the same invalidation contract as the reference.
+
+Every vector lives on the GPU in a padded buffer.  The public attributes
+(``u``, ``v``, ``log_rP``, ``row_sums()`` ...) return host numpy copies so code
+written against the reference keeps working; the solver itself only touches
+the device buffers (``_u``, ``_lr`` ...).  The op tally is incremented at the
+reference's call sites (``dual.py:73,87,95,97,163,173,181,191,205``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib, opcount
+from ._device import DeviceCost, is_tensor, require_cuda, torch, vptr
+from .errors import DomainError
+
+
+def device_cost(problem, device=None):
+    """The problem's device-resident cost, created once per problem object."""
+    dc = getattr(problem, "_otn_device_cost", None)
+    dev = require_cuda(device)
+    if dc is None or dc.ctx.device != dev:
+        dc = DeviceCost(problem, dev)
+        try:
+            problem._otn_device_cost = dc
+        except AttributeError:
+            pass
+    else:
+        dc.ctx.sync_stream()
+    return dc
+
+
+class DualState:
+    """Single-owner mutable dual state at one temperature (dual.py:22-46)."""
+
+    def __init__(self, problem, gamma, u=None, v=None, r=None, c=None, *, cost=None):
+        if not np.isfinite(gamma) or gamma <= 0.0:
+            raise DomainError(f"gamma must be positive and finite, got {gamma}")
+        self.problem = problem
+        self._dc = cost if cost is not None else device_cost(problem)
+        self._ctx = self._dc.ctx
+        k = self._ctx
+        self._gamma = float(gamma)
+        self._u = k.vec(np.zeros(self.n) if u is None else u)
+        self._v = k.vec(np.zeros(self.n) if v is None else v)
+        self._lr = k.vec()
+        self._lc = k.vec()
+        self._g = k.vec()
+        self._trial_vec = k.vec()
+        self._tmp = k.vec()
+        self._cache_valid = False
+        self._rowstat = None
+        self._K_formed = False
+        self._KT_formed = False
+        self._plan_buf = None
+        self.set_targets(problem.r if r is None else r, problem.c if c is None else c)
+
+    # -- invalidating attributes (dual.py:48-54) ----------------------------
+    @property
+    def n(self):
+        return self.problem.n
+
+    @property
+    def gamma(self):
+        return self._gamma
+
+    @gamma.setter
+    def gamma(self, value):
+        self._gamma = float(value)
+        self._cache_valid = False
+        self._rowstat = None
+        self._K_formed = False
+        self._KT_formed = False
+
+    @property
+    def u(self):
+        return self._ctx.download(self._u)
+
+    @u.setter
+    def u(self, value):
+        self._ctx.upload(self._u, value)
+        self._invalidate()
+
+    @property
+    def v(self):
+        return self._ctx.download(self._v)
+
+    @v.setter
+    def v(self, value):
+        self._ctx.upload(self._v, value)
+        self._invalidate()
+
+    def _invalidate(self):
+        self._cache_valid = False
+        self._rowstat = None
+
+    @property
+    def cache_valid(self):
+        return self._cache_valid
+
+    def set_targets(self, r, c):
+        """Swap the target marginals (dual.py:64-67); logs are taken on the host
+        with numpy, exactly as the reference's np.log(r) / np.log(c)."""
+        self.r = np.asarray(r, dtype=np.float64)
+        self.c = np.asarray(c, dtype=np.float64)
+        k = self._ctx
+        self._r = k.vec(self.r)
+        self._c = k.vec(self.c)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            self._log_r = k.vec(np.log(self.r))
+            self._log_c = k.vec(np.log(self.c))
+        self._rowstat = None
+
+    # -- op tally for the implicit K = -gamma C and its transpose -----------
+    @property
+    def _ng(self):
+        return -self._gamma
+
+    def _touch_K(self):
+        if not self._K_formed:
+            opcount.add(1)          # dual.py:73
+            self._K_formed = True
+
+    def _touch_KT(self):
+        if not self._KT_formed:
+            self._touch_K()
+            if not self._dc.symmetric:
+                opcount.add(1)      # dual.py:87
+            self._KT_formed = True
+
+    # -- device kernels --------------------------------------------------------
+    def _lse_rows(self, outer, inner, out):
+        self._touch_K()
+        self._ctx.call("otn_lse_rows", self._dc.ptr(), self._ng, vptr(outer), vptr(inner),
+                       vptr(out))
+
+    def _lse_cols(self, outer, inner, out):
+        self._touch_KT()
+        self._ctx.call("otn_lse_cols", self._dc.ptr(), int(self._dc.symmetric), self._ng,
+                       vptr(outer), vptr(inner), vptr(out))
+
+    def refresh(self):
+        """Recompute both cached log sums (dual.py:91-102)."""
+        if not np.isfinite(self._gamma):
+            raise DomainError("gamma must be finite")
+        opcount.add(4)
+        self._lse_rows(self._u, self._v, self._lr)
+        opcount.add(4)
+        self._lse_cols(self._v, self._u, self._lc)
+        self._cache_valid = True
+        self._rowstat = None
+
+    def refresh_row_sums(self):
+        self.refresh()
+        return self.log_rP
+
+    def _lr_dev(self):
+        if not self._cache_valid:
+            self.refresh()
+        return self._lr
+
+    def _lc_dev(self):
+        if not self._cache_valid:
+            self.refresh()
+        return self._lc
+
+    @property
+    def log_rP(self):
+        return self._ctx.download(self._lr_dev())
+
+    @property
+    def log_cP(self):
+        return self._ctx.download(self._lc_dev())
+
+    def set_log_row_sums(self, log_rP):
+        self._ctx.upload(self._lr, log_rP)
+        self._rowstat = None
+
+    def set_log_col_sums(self, log_cP):
+        self._ctx.upload(self._lc, log_cP)
+
+    def mark_cache_valid(self):
+        self._cache_valid = True
+
+    def row_sums(self):
+        return np.exp(self.log_rP)
+
+    def col_sums(self):
+        return np.exp(self.log_cP)
+
+    # -- derived quantities (device reductions) ---------------------------------
+    def _row_stats(self):
+        """(||exp(log_rP) - r||_1, sum r^2/exp(log_rP), flags); g = exp(log_rP) - r
+        is left in self._g.  Cached until log_rP or r changes."""
+        if self._rowstat is None:
+            lr = self._lr_dev()
+            k = self._ctx
+            k.call("otn_vec", _lib.VEC_GRAD, 0.0, vptr(lr), vptr(self._r), None, None,
+                   vptr(self._g))
+            out = (ctypes.c_double * 2)()
+            fl = ctypes.c_int(0)
+            k.call("otn_reduce", _lib.RED_ROW_STATS, vptr(lr), vptr(self._r), None, None, out,
+                   ctypes.byref(fl))
+            self._rowstat = (float(out[0]), float(out[1]), int(fl.value))
+        return self._rowstat
+
+    def _row_grad_norm(self):
+        return self._row_stats()[0]
+
+    def _chi_sq(self):
+        """chi_sq_div(r, row_sums()) (core.py:42-52) with its domain checks."""
+        _, s, fl = self._row_stats()
+        if fl & 1:
+            raise DomainError("chi_sq_div requires strictly positive reference x")
+        if fl & 2:
+            raise DomainError("chi_sq_div requires nonnegative y")
+        return float(s - 1.0)
+
+    def gradient(self):
+        """(grad_u, grad_v) = (r(P) - r, c(P) - c) as host arrays (dual.py:142-144)."""
+        return self.row_sums() - self.r, self.col_sums() - self.c
+
+    def grad_norm_l1(self):
+        """||r(P) - r||_1 + ||c(P) - c||_1 on the device (dual.py:146-148)."""
+        out = (ctypes.c_double * 2)()
+        self._ctx.call("otn_reduce", _lib.RED_GRAD_L1, vptr(self._lr_dev()), vptr(self._r),
+                       vptr(self._lc_dev()), vptr(self._c), out, None)
+        return float(out[0] + out[1])
+
+    def dual_value(self):
+        """sum(P) - 1 - <u, r> - <v, c> (dual.py:150-153)."""
+        k = self._ctx
+        out = (ctypes.c_double * 2)()
+        k.call("otn_reduce", _lib.RED_SUM_EXP, vptr(self._lr_dev()), None, None, None, out, None)
+        mass = float(out[0])
+        k.call("otn_reduce", _lib.RED_DOT, vptr(self._u), vptr(self._r), None, None, out, None)
+        ur = float(out[0])
+        k.call("otn_reduce", _lib.RED_DOT, vptr(self._v), vptr(self._c), None, None, out, None)
+        vc = float(out[0])
+        return mass - 1.0 - ur - vc
+
+    # -- plan --------------------------------------------------------------------
+    def _materialize(self, reuse_buffer=False, icP=None, rP=None, mu=None, check=True):
+        """Device plan P (n x ld); optional fused Jacobi diagonal (K4 + K5)."""
+        opcount.add(4)
+        self._touch_K()
+        k = self._ctx
+        if reuse_buffer:
+            if self._plan_buf is None:
+                self._plan_buf = k.mat()
+            P = self._plan_buf
+        else:
+            P = k.mat()
+        flag = ctypes.c_int(0)
+        rc = k.call("otn_materialize", self._dc.ptr(), self._ng, vptr(self._u), vptr(self._v),
+                    vptr(P), vptr(icP), vptr(rP), vptr(mu),
+                    ctypes.byref(flag) if check else None)
+        if rc == _lib.OTN_ST_PLAN_OVERFLOW:
+            _lib.raise_for_status(rc, "materialize_plan")
+        return P
+
+    def materialize_plan(self, reuse_buffer=False):
+        """Linear-domain plan (dual.py:155-169); host array for host problems."""
+        P = self._materialize(reuse_buffer=reuse_buffer)
+        if is_tensor(self.problem.C):
+            return P[:, : self.n]
+        return P[:, : self.n].cpu().numpy()
+
+    def _trial(self, d_u, d_v, alpha, out):
+        """Trial log column sums at (u + alpha d_u, v + alpha d_v) and the plan
+        mass (dual.py:171-175 + projector.py:122-126); returns the mass."""
+        opcount.add(4)
+        self._touch_KT()
+        mass = ctypes.c_double(0.0)
+        self._ctx.call("otn_trial_cols", self._dc.ptr(), int(self._dc.symmetric), self._ng,
+                       vptr(self._u), vptr(d_u), vptr(self._v), vptr(d_v), float(alpha),
+                       vptr(out), ctypes.byref(mass))
+        return float(mass.value)
+
+    def _trial_buf(self):
+        return self._trial_vec
+
+    def trial_log_col_sums(self, d_u, d_v, alpha):
+        k = self._ctx
+        du = d_u if is_tensor(d_u) else k.vec(d_u)
+        dv = d_v if is_tensor(d_v) else k.vec(d_v)
+        out = k.vec()
+        self._trial(du, dv, alpha, out)
+        return k.download(out)
+
+    # -- exact scaling updates (dual.py:179-208) --------------------------------
+    def rebalance_columns(self):
+        """v = log c - LSE_cols(u); log c(P) := log c; refresh rows (dual.py:179-184)."""
+        opcount.add(4)
+        self._touch_KT()
+        self._ctx.call("otn_rebalance_cols", self._dc.ptr(), int(self._dc.symmetric), self._ng,
+                       vptr(self._log_c), vptr(self._u), vptr(self._v))
+        self._invalidate()
+        self._lc.copy_(self._log_c)
+        self.refresh_rows_only()
+
+    def scale_rows_to_target(self):
+        """u += log r - log r(P); log r(P) := log r; column cache (dual.py:186-194)."""
+        lr = self._lr_dev()
+        self._ctx.call("otn_vec", _lib.VEC_ADD_SUB, 0.0, vptr(self._u), vptr(self._log_r),
+                       vptr(lr), None, vptr(self._u))
+        self._invalidate()
+        self._lr.copy_(self._log_r)
+        opcount.add(4)
+        self._lse_cols(self._v, self._u, self._lc)
+        self._cache_valid = True
+
+    def scale_cols_to_target(self):
+        """v += log c - log c(P); log c(P) := log c; refresh rows (dual.py:196-201)."""
+        lc = self._lc_dev()
+        self._ctx.call("otn_vec", _lib.VEC_ADD_SUB, 0.0, vptr(self._v), vptr(self._log_c),
+                       vptr(lc), None, vptr(self._v))
+        self._invalidate()
+        self._lc.copy_(self._log_c)
+        self.refresh_rows_only()
+
+    def refresh_rows_only(self):
+        """log r(P) = LSE_rows, column cache assumed current (dual.py:203-208)."""
+        opcount.add(4)
+        self._lse_rows(self._u, self._v, self._lr)
+        self._rowstat = None
+        self._cache_valid = True
+
+    # -- stacked potentials (dual.py:212-219) ------------------------------------
+    @property
+    def z(self):
+        return np.concatenate([self.u, self.v])
+
+    def set_z(self, z):
+        n = self.n
+        if is_tensor(z):
+            self._u[:n].copy_(z[:n])
+            self._v[:n].copy_(z[n:])
+            self._invalidate()
+        else:
+            self.u = np.asarray(z[:n], dtype=np.float64)
+            self.v = np.asarray(z[n:], dtype=np.float64)
+
+    def _z_dev(self):
+        """Device copy of (u, v) for the annealing driver's extrapolation."""
+        return self._u.clone(), self._v.clone()

@@ -1,0 +1,258 @@
+"""The discounted Newton system and its device-resident solvers (mirrors ``newton.py``).
+
+``F(rho) = D(rP) (I - rho P_rc)`` with ``P_rc = D(rP)^-1 P D(cP)^-1 P^T`` is
+applied as two streaming passes over the plan in HBM (K6, K7).  ``pcg_solve``
+and ``newton_solve`` each run as ONE persistent cooperative kernel
+(``otn_pcg`` / ``otn_newton``): the CG loop, the 50-iteration true-residual
+refresh, the L1 stopping test, the forcing test and the rho annealing all
+happen on the device; the host reads back only the outcome record.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, opcount
+from ._device import Context, is_tensor, require_cuda, vptr
+from .errors import ConditioningError, NonconvergenceError, StagnationError
+
+RHO_CAP = 1e-12               # newton.py:32
+RHO_DECAY = 4.0               # newton.py:34
+CG_TOL_FRACTION = 0.25        # newton.py:36
+TRUE_RESIDUAL_REFRESH = 50    # newton.py:38 (compiled into the kernel)
+
+
+@dataclass
+class NewtonResult:
+    """Outcome of one annealed truncated-Newton direction solve (newton.py:59-66)."""
+
+    d_u: object
+    rho_final: float
+    cg_iters: int
+    undiscounted_residual_l1: float
+
+
+def _as_host(like, dev_vec, ctx):
+    """Return dev_vec in the caller's array type (numpy in -> numpy out)."""
+    if is_tensor(like):
+        return dev_vec[: ctx.n].clone()
+    return ctx.download(dev_vec)
+
+
+class DiscountedSystem:
+    """Plan snapshot realizing P_rc, P_c and F(rho) as device operators.
+
+    Constructed either from host/device arrays (API parity with newton.py:72-79)
+    or, on the solver path, from a DualState via :meth:`from_state`, which
+    materializes the plan into the state's reusable HBM buffer together with
+    the Jacobi diagonal (one fused pass, K4 + K5).
+    """
+
+    def __init__(self, P, rP, cP, *, _ctx=None, _mu=None, _icP=None):
+        if _ctx is None:
+            rP_h = rP.detach().cpu().numpy() if is_tensor(rP) else np.asarray(rP, dtype=np.float64)
+            cP_h = cP.detach().cpu().numpy() if is_tensor(cP) else np.asarray(cP, dtype=np.float64)
+            if np.any(rP_h <= 0.0) or np.any(cP_h <= 0.0):
+                raise ConditioningError("plan row/column sums must be strictly positive")
+            n = int(P.shape[0])
+            ctx = Context.get(n, require_cuda(P.device if is_tensor(P) else None))
+            Pd = ctx.mat()
+            if is_tensor(P):
+                Pd[:, : min(P.shape[1], ctx.ld)].copy_(P[:, : ctx.ld])
+            else:
+                from ._device import torch
+                Pd[:, :n].copy_(torch().from_numpy(np.ascontiguousarray(P, dtype=np.float64)))
+            self._ctx = ctx
+            self._P = Pd
+            self._rP = ctx.vec(rP_h)
+            self._cP = ctx.vec(cP_h)
+            self._icP = ctx.vec(1.0 / cP_h)
+            self._mu_dev = None
+        else:
+            self._ctx = _ctx
+            self._P, self._rP, self._cP = P, rP, cP
+            self._icP = _icP
+            self._mu_dev = _mu
+        self.n = self._ctx.n
+        self._mu_counted = False
+
+    @classmethod
+    def from_state(cls, state):
+        """Snapshot the current plan (newton.py:81-90): rP, cP from the log-domain
+        caches, P into the state's reusable buffer, mu fused into that pass."""
+        ctx = state._ctx
+        bufs = getattr(state, "_sysbufs", None)
+        if bufs is None:
+            bufs = tuple(ctx.vec() for _ in range(4))
+            state._sysbufs = bufs
+        rP, cP, icP, mu = bufs
+        lr, lc = state._lr_dev(), state._lc_dev()
+        ctx.call("otn_system_prep", vptr(lr), vptr(lc), vptr(rP), vptr(cP), vptr(icP), None)
+        P = state._materialize(reuse_buffer=True, icP=icP, rP=rP, mu=mu, check=False)
+        flags = (ctypes.c_int * 4)()
+        ctx.call("otn_read_flags", flags)
+        if flags[0]:
+            _lib.raise_for_status(_lib.OTN_ST_PLAN_OVERFLOW, "materialize_plan")
+        if flags[1]:
+            _lib.raise_for_status(_lib.OTN_ST_NONPOSITIVE_SUMS, "DiscountedSystem")
+        return cls(P, rP, cP, _ctx=ctx, _mu=mu, _icP=icP)
+
+    # -- host views for API parity ---------------------------------------------
+    @property
+    def P(self):
+        return self._P[:, : self.n].cpu().numpy()
+
+    @property
+    def rP(self):
+        return self._ctx.download(self._rP)
+
+    @property
+    def cP(self):
+        return self._ctx.download(self._cP)
+
+    def _in(self, d):
+        if is_tensor(d):
+            if d.shape[0] >= self._ctx.ld and d.is_contiguous():
+                return d
+            return self._ctx.vec(d)
+        return self._ctx.vec(d)
+
+    # -- operators (newton.py:92-112) ------------------------------------------------
+    def apply_pc(self, d):
+        """P_c d = (P^T d)/cP (newton.py:96-98)."""
+        opcount.add(1)
+        out = self._ctx.vec()
+        self._ctx.call("otn_apply_pc", vptr(self._P), vptr(self._cP), vptr(self._in(d)), vptr(out))
+        return _as_host(d, out, self._ctx)
+
+    def apply_prc(self, d):
+        """P_rc d = P((P^T d)/cP)/rP (newton.py:92-94)."""
+        opcount.add(2)
+        k = self._ctx
+        w = k.vec()
+        k.call("otn_apply_pc", vptr(self._P), vptr(self._cP), vptr(self._in(d)), vptr(w))
+        s = k.vec()
+        k.call("otn_matvec", vptr(self._P), vptr(w), vptr(s))
+        out = s / self._rP.clamp_min(np.finfo(np.float64).tiny)
+        return _as_host(d, out, k)
+
+    def apply_F(self, rho, d):
+        """F(rho) d = rP*d - rho*P((P^T d)/cP) (newton.py:100-105)."""
+        if rho != 0.0:
+            opcount.add(2)
+        out = self._ctx.vec()
+        self._ctx.call("otn_apply_F", vptr(self._P), vptr(self._rP), vptr(self._cP), float(rho),
+                       vptr(self._in(d)), vptr(out))
+        return _as_host(d, out, self._ctx)
+
+    def _tally_mu(self):
+        if not self._mu_counted:
+            opcount.add(2)
+            self._mu_counted = True
+
+    def _mu(self):
+        if self._mu_dev is None:
+            k = self._ctx
+            self._mu_dev = k.vec()
+            sq = k.vec()
+            k.call("otn_square_matvec", vptr(self._P), vptr(self._icP), vptr(sq))
+            self._mu_dev[: self.n] = sq[: self.n] / self._rP[: self.n]
+        return self._mu_dev
+
+    def diag_prc(self):
+        """mu = diag(P_rc) = ((P*P) @ (1/cP)) / rP (newton.py:107-112)."""
+        self._tally_mu()
+        return self._ctx.download(self._mu())
+
+    def dense_prc(self):
+        """Dense P_rc for small-n validation (newton.py:116-117); host numpy."""
+        P, rP, cP = self.P, self.rP, self.cP
+        return (P / rP[:, None]) @ (P.T / cP[:, None])
+
+    def dense_F(self, rho):
+        return np.diag(self.rP) @ (np.eye(self.n) - rho * self.dense_prc())
+
+
+def _finish(res, what, best, rho_for_msg=None, eta_gn=None):
+    rc = res.status
+    if rc == _lib.OTN_OK:
+        return
+    diag = {"rho": res.diag_rho, "residual_l1": res.diag_resid}
+    if rc == _lib.OTN_ST_NONCONVERGENCE:
+        raise NonconvergenceError("CG did not reach its tolerance within the iteration budget",
+                                  best=best() if best else None, diagnostics=diag)
+    if rc == _lib.OTN_ST_STAGNATION:
+        raise StagnationError(
+            f"discount reached {res.diag_rho} without meeting the forcing test "
+            f"(residual {res.resid_l1:.3g} > {eta_gn:.3g})")
+    if rc == _lib.OTN_ST_BREAKDOWN:
+        raise ConditioningError(f"CG breakdown: curvature {res.diag_resid:.3g} along search direction")
+    _lib.raise_for_status(rc, what)
+
+
+def pcg_solve(sys, rho, b, tol_l1, d0=None, max_iters=None):
+    """Jacobi-PCG for F(rho) d = b on the device (newton.py:123-172).
+
+    Returns ``(d, iterations)`` in the caller's array type.
+    """
+    if not 0.0 <= rho < 1.0:
+        raise ConditioningError(f"pcg_solve needs rho in [0, 1), got {rho}")
+    if tol_l1 <= 0.0:
+        raise ConditioningError("tol_l1 must be positive")
+    if max_iters is None:
+        max_iters = 10 * sys.n
+    k = sys._ctx
+    sys._tally_mu()
+    mu = sys._mu()
+    bd = sys._in(b)
+    x = k.vec(d0) if d0 is not None else k.vec()
+    res = _lib.SolveResult()
+    rc = k.call("otn_pcg", vptr(sys._P), vptr(sys._rP), vptr(sys._cP), vptr(mu), float(rho),
+                vptr(bd), float(tol_l1), vptr(x), int(d0 is not None), int(max_iters),
+                ctypes.byref(res))
+    opcount.add(2 * int(res.hvps))
+    like = b if d0 is None else d0
+    _finish(res if rc == res.status else res, "pcg_solve",
+            best=lambda: _as_host(like, x, k))
+    return _as_host(like, x, k), int(res.cg_iters)
+
+
+def _newton_device(grad_u, sys, eta, rho0, zero_init, max_cg_iters, d_u, d_v):
+    """One otn_newton launch; op tally as the reference's call pattern."""
+    k = sys._ctx
+    if max_cg_iters is None:
+        max_cg_iters = 10 * sys.n
+    res = _lib.SolveResult()
+    k.call("otn_newton", vptr(sys._P), vptr(sys._rP), vptr(sys._cP), vptr(sys._mu()),
+           vptr(grad_u), float(eta), float(rho0), int(bool(zero_init)), int(max_cg_iters),
+           vptr(d_u), vptr(d_v), ctypes.byref(res))
+    if res.pcg_calls > 0:
+        sys._tally_mu()
+    opcount.add(2 * int(res.hvps))
+    return res
+
+
+def newton_solve(grad_u, sys, eta, rho0=0.0, zero_init=False, max_cg_iters=None):
+    """Annealed discounted solve for the truncated Newton direction (newton.py:175-210)."""
+    if eta <= 0.0:
+        raise ConditioningError(f"eta must be positive, got {eta}")
+    if not 0.0 <= rho0 < 1.0:
+        raise ConditioningError(f"rho0 must be in [0, 1), got {rho0}")
+    k = sys._ctx
+    g = sys._in(grad_u)
+    d = k.vec()
+    res = _newton_device(g, sys, eta, rho0, zero_init, max_cg_iters, d, None)
+    gn = float(np.abs(k.download(g)).sum()) if res.status == _lib.OTN_ST_STAGNATION else 0.0
+    _finish(res, "newton_solve", best=lambda: _as_host(grad_u, d, k), eta_gn=eta * gn)
+    return NewtonResult(_as_host(grad_u, d, k), float(res.rho_final), int(res.cg_iters),
+                        float(res.resid_l1))
+
+
+def next_rho0(rho_old):
+    """Warm-start discount for the next solve (newton.py:213-217)."""
+    if not 0.0 <= rho_old < 1.0:
+        raise ConditioningError(f"rho_old must be in [0, 1), got {rho_old}")
+    return max(0.0, 1.0 - (1.0 - rho_old) * RHO_DECAY)

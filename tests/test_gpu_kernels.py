@@ -1,0 +1,184 @@
+"""Kernel-level parity on the B200: each C-ABI operator vs the CPU oracle on the
+same seeded inputs (tolerances written per test: float64, different but fixed
+reduction trees, so agreement is at the 1e-15..1e-13 relative level)."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import otn_oracle as orc
+from paper_2504_02067_b200 import DiscountedSystem, DualState, newton_solve, pcg_solve, problems
+from paper_2504_02067_b200.errors import (
+    ConditioningError,
+    NonconvergenceError,
+    PlanOverflowError,
+)
+
+pytestmark = pytest.mark.gpu
+
+LSE_RTOL = 1e-13   # log-sum-exp: online (max, sum) merge vs numpy pairwise sum
+
+
+def make_state(n, seed=0, gamma=4.0, spread=0.5, metric="l1", symmetric=True):
+    if symmetric:
+        C = problems.grid_points_cost(n, metric)
+    else:
+        rng = np.random.default_rng(seed + 99)
+        C = rng.random((n, n))
+    r = problems.gen_marginal(n, "smooth-random", seed)
+    c = problems.gen_marginal(n, "spiky-random", seed + 100)
+    prob = problems.Problem(C=C, r=r, c=c)
+    rng = np.random.default_rng(seed + 1)
+    u = np.log(r) + spread * rng.standard_normal(n)
+    v = np.log(c) + spread * rng.standard_normal(n)
+    return prob, u, v
+
+
+def oracle_state(prob, gamma, u, v):
+    return orc.Dual(prob.C, gamma, u, v, prob.r, prob.c, orc.Tally())
+
+
+@pytest.mark.parametrize("n,sym", [(1, True), (5, True), (33, True), (273, True), (273, False),
+                                   (1000, False), (4096, True)])
+def test_row_and_column_lse(n, sym):
+    prob, u, v = make_state(n, seed=n, symmetric=sym)
+    gamma = 37.5
+    st = DualState(prob, gamma, u=u, v=v)
+    ref = oracle_state(prob, gamma, u, v)
+    np.testing.assert_allclose(st.log_rP, ref.log_r, rtol=LSE_RTOL, atol=1e-300)
+    np.testing.assert_allclose(st.log_cP, ref.log_c, rtol=LSE_RTOL, atol=1e-300)
+
+
+def test_lse_large_magnitude_and_tail():
+    """No overflow at |x| ~ 1000 (test_core.py:17-19); n not a tile multiple."""
+    n = 257
+    prob, u, v = make_state(n, seed=3)
+    u = u + 1000.0
+    st = DualState(prob, 2.0, u=u, v=v)
+    ref = oracle_state(prob, 2.0, u, v)
+    np.testing.assert_allclose(st.log_rP, ref.log_r, rtol=LSE_RTOL)
+    np.testing.assert_allclose(st.log_cP, ref.log_c, rtol=LSE_RTOL)
+
+
+def test_rebalance_and_exit_scaling():
+    prob, u, v = make_state(300, seed=7, symmetric=False)
+    st = DualState(prob, 8.0, u=u, v=v)
+    ref = oracle_state(prob, 8.0, u, v)
+    st.rebalance_columns()
+    ref.balance_cols()
+    np.testing.assert_allclose(st.v, ref.v, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(st.log_rP, ref.log_r, rtol=1e-13, atol=1e-13)
+    st.scale_rows_to_target()
+    ref.balance_rows_exit()
+    np.testing.assert_allclose(st.u, ref.u, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(st.log_cP, ref.log_c, rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("sym", [True, False])
+def test_trial_column_sums_and_mass(sym):
+    n = 500
+    prob, u, v = make_state(n, seed=11, symmetric=sym)
+    st = DualState(prob, 6.0, u=u, v=v)
+    ref = oracle_state(prob, 6.0, u, v)
+    rng = np.random.default_rng(0)
+    du, dv = rng.standard_normal(n), rng.standard_normal(n)
+    got = st.trial_log_col_sums(du, dv, 0.3)
+    want = ref.trial_log_c(du, dv, 0.3)
+    np.testing.assert_allclose(got, want, rtol=LSE_RTOL)
+
+
+def test_materialize_and_mu():
+    n = 700
+    prob, u, v = make_state(n, seed=5)
+    st = DualState(prob, 12.0, u=u, v=v)
+    ref = oracle_state(prob, 12.0, u, v)
+    P = st.materialize_plan()
+    np.testing.assert_allclose(P, ref.plan(), rtol=2e-15, atol=0)
+    sysd = DiscountedSystem.from_state(st)
+    sysr = orc.System.of(ref)
+    np.testing.assert_allclose(sysd.diag_prc(), sysr.mu(), rtol=1e-13)
+    np.testing.assert_allclose(sysd.rP, sysr.rP, rtol=1e-13)
+
+
+def test_overflow_rejected():
+    prob, u, v = make_state(3)
+    st = DualState(prob, 4.0, u=u + 800.0, v=v)
+    with pytest.raises(PlanOverflowError):
+        st.materialize_plan()
+
+
+@pytest.mark.parametrize("n", [8, 300, 4096])
+def test_hvp_operators(n):
+    prob, u, v = make_state(n, seed=2, gamma=4.0)
+    st = DualState(prob, 4.0, u=u, v=v)
+    sysd = DiscountedSystem.from_state(st)
+    P, rP, cP = sysd.P, sysd.rP, sysd.cP
+    d = np.random.default_rng(1).standard_normal(n)
+    for rho in (0.0, 0.5, 1.0):
+        want = rP * d - rho * (P @ ((P.T @ d) / cP))
+        np.testing.assert_allclose(sysd.apply_F(rho, d), want, rtol=1e-12, atol=1e-14 * np.abs(want).max())
+    np.testing.assert_allclose(sysd.apply_pc(d), (P.T @ d) / cP, rtol=1e-12)
+    np.testing.assert_allclose(sysd.apply_prc(d), (P @ ((P.T @ d) / cP)) / rP, rtol=1e-12)
+
+
+@pytest.mark.parametrize("n_,seed", [(32, 33), (64, 3), (256, 5)])
+def test_pcg_and_newton_vs_reference(kernels_golden, n_, seed):
+    """CG iteration counts exact, solutions to 1e-10 relative vs the reference."""
+    g = kernels_golden
+    C = problems.grid_points_cost(n_, "l1")
+    r = problems.gen_marginal(n_, "smooth-random", seed)
+    c = problems.gen_marginal(n_, "spiky-random", seed + 100)
+    rs = np.random.default_rng(seed + 7)
+    st = DualState(problems.Problem(C=C, r=r, c=c), 4.0,
+                   u=np.log(r) + 0.3 * rs.standard_normal(n_),
+                   v=np.log(c) + 0.3 * rs.standard_normal(n_))
+    sysd = DiscountedSystem.from_state(st)
+    np.testing.assert_allclose(sysd.diag_prc(), g[f"sys{n_}_mu"], rtol=1e-13)
+    b = np.random.default_rng(seed + 1).standard_normal(n_) * 0.01
+    for rho in (0.0, 0.9, 0.99):
+        x, it = pcg_solve(sysd, rho, b, 1e-12)
+        ref = g[f"sys{n_}_pcg{rho}_x"]
+        assert it == int(g[f"sys{n_}_pcg{rho}_iters"][0])
+        assert np.abs(x - ref).max() <= 1e-10 * np.abs(ref).max()
+    res = newton_solve(b - b.mean(), sysd, 0.05)
+    meta = g[f"sys{n_}_newton_meta"]
+    assert res.cg_iters == int(meta[1])
+    assert res.rho_final == meta[0]
+    ref = g[f"sys{n_}_newton_d"]
+    assert np.abs(res.d_u - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+def test_pcg_warm_start_and_budget():
+    prob, u, v = make_state(32, seed=35)
+    sysd = DiscountedSystem.from_state(DualState(prob, 4.0, u=u, v=v))
+    b = np.random.default_rng(36).standard_normal(32)
+    d, _ = pcg_solve(sysd, 0.7, b, tol_l1=1e-12)
+    d2, iters = pcg_solve(sysd, 0.7, b, tol_l1=1e-10, d0=d)
+    assert iters == 0
+    np.testing.assert_array_equal(d2, d)
+    with pytest.raises(NonconvergenceError) as err:
+        pcg_solve(sysd, 0.9999, b, tol_l1=1e-15, max_iters=2)
+    assert err.value.best is not None and err.value.best.shape == (32,)
+    with pytest.raises(ConditioningError):
+        pcg_solve(sysd, 1.0, b, tol_l1=1e-10)
+
+
+def test_jacobi_exact_direction_and_hand_mu():
+    sysd = DiscountedSystem(np.full((2, 2), 0.25), np.array([0.5, 0.5]), np.array([0.5, 0.5]))
+    np.testing.assert_allclose(sysd.diag_prc(), [0.5, 0.5], rtol=1e-15)
+    res = newton_solve(np.array([-0.1, 0.1]), sysd, eta=0.25, rho0=0.0)
+    np.testing.assert_allclose(res.d_u, [0.2, -0.2], rtol=1e-14)
+    assert res.cg_iters == 0 and res.rho_final == 0.0
+
+
+def test_rho_anneals_on_quarter_grid():
+    prob, u, v = make_state(16, seed=41)
+    sysd = DiscountedSystem.from_state(DualState(prob, 16.0, u=u, v=v))
+    grad = np.random.default_rng(42).standard_normal(16) * 0.01
+    grad -= grad.mean()
+    res = newton_solve(grad, sysd, eta=0.01)
+    k = math.log(1.0 - res.rho_final) / math.log(4.0)
+    assert k == pytest.approx(round(k), abs=1e-9)
+    resid = sysd.apply_F(1.0, res.d_u) + grad
+    assert np.abs(resid).sum() <= 0.01 * np.abs(grad).sum() + 1e-15
