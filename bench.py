@@ -1,0 +1,376 @@
+"""Benchmark: time to precision of the truncated-Newton EOT solver (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (configs[1] of BASELINE.json, the metric's configuration): D2, n = 4096
+(64x64 pixel grid), squared-L2 cost, smooth-random marginals (seeds 0 / 1),
+MDOT annealing gamma 2^5 -> 2^16 until ||r(P)-r||_1 + ||c(P)-c||_1 <= 1e-6.
+One step = one complete ``mdot`` solve (all stages, final plan, rounding,
+primal cost).  The metric is seconds per solve (lower is better).
+
+  value  device-resident: C already in HBM (a CUDA tensor problem); CUDA
+         events bracket each solve on the solver stream; L2 is flushed
+         (512 MB write) between steps, and the 134 MB cost is itself > L2.
+  e2e    the same solve through the public API with a HOST numpy problem:
+         the 134 MB cost H2D, the solve, and the 134 MB rounded plan D2H all
+         inside the timed region (bytes counted by the package).
+  roofline  the persistent CG/Newton kernel (k_coop), the dominant kernel:
+         algorithmic bytes = 16 n^2 per Hessian-vector product (two streaming
+         passes over the plan) + 8 n^2 for the d_v back-substitution, summed
+         over the launches of the timed region / their summed CUDA-event time.
+  cpu_baseline  the bit-exact oracle port of the reference (oracle/), all host
+         threads for BLAS: a bounded sample of each dense primitive on the
+         same n = 4096 problem, scaled by the reference's own primitive-call
+         counts for this solve (tests/golden/callmix_*.json).
+
+Multi-GPU (--gpus N under torchrun): replicas only — the n = 4096 solve does
+not shard profitably; each rank solves its own seed, value is the
+max-over-ranks time per solve divided by N (whole-job seconds per solve).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = dict(spec="grid:64:l2sq:{seed}", gamma_i=2.0 ** 5, gamma_f=2.0 ** 16, p=1.5, q_init=2.0)
+CALLMIX = os.path.join(ROOT, "tests", "golden", "callmix_D2_grid64_l2sq_s0.json")
+METRIC = "sec to ||r(P)-r||_1+||c(P)-c||_1<=1e-6 (n=4096)"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world):
+    import torch
+
+    import paper_2504_02067_b200 as ot
+    from paper_2504_02067_b200._device import TELEMETRY
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    seed = rank  # replicas: one seed per rank
+    host_prob = ot.workload(WORKLOAD["spec"].format(seed=seed))
+    n = host_prob.n
+    dprob = ot.Problem(C=torch.from_numpy(host_prob.C).to(dev), r=host_prob.r, c=host_prob.c,
+                       label=host_prob.label)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def solve(prob):
+        return ot.mdot(prob, WORKLOAD["gamma_i"], WORKLOAD["gamma_f"], p=WORKLOAD["p"],
+                       q_init=WORKLOAD["q_init"])
+
+    for _ in range(args.warmup):
+        solve(dprob)
+    torch.cuda.synchronize()
+    barrier(world)
+
+    # ---- device-resident timed region ------------------------------------
+    TELEMETRY.reset()
+    TELEMETRY.time_coop = True
+    step_ms = []
+    sols = []
+    with ClockSampler(dev.index) as clocks:
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.fill_(1.0)                         # evict L2 between steps (untimed)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sols.append(solve(dprob))
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+    TELEMETRY.time_coop = False
+    launches = TELEMETRY.launches
+    coop = list(TELEMETRY.coop)
+    calls = dict(TELEMETRY.calls)
+    barrier(world)
+
+    # ---- e2e through the public API with host buffers ------------------------
+    TELEMETRY.reset()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sol_h = solve(host_prob)          # H2D of C inside, D2H of the rounded P inside
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    h2d = TELEMETRY.h2d / args.steps
+    d2h = TELEMETRY.d2h / args.steps
+
+    # ---- precision check of the timed solves (after the timed region) -----
+    errs = []
+    for s in sols[:1] + [sol_h]:
+        st = s.final_state
+        st.set_targets(host_prob.r, host_prob.c)
+        errs.append(st.grad_norm_l1())
+
+    # ---- roofline of the dominant kernel -------------------------------------
+    nn8 = float(n) * n * 8.0            # one pass over the n x n float64 plan
+    alg_bytes = sum(2.0 * nn8 * h + nn8 * dv for (_, _, h, dv, _) in coop)
+    coop_ms = sum(a.elapsed_time(b) for (a, b, _, _, _) in coop)
+    hbm, hbm_src = peaks()
+    achieved = alg_bytes / (coop_ms * 1e-3) / 1e9 if coop_ms > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "kcoop_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("traffic_bytes_per_alg_byte")
+
+    ms = max_over_ranks(statistics.mean(step_ms), world)
+    e2e = max_over_ranks(statistics.mean(e2e_ms), world)
+    out = {
+        "metric": METRIC,
+        "value": ms / 1e3 / world,
+        "unit": "s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded 64x64 grid cost + smooth-random marginals, reference generators)",
+        "config": {"workload": "D2 n=4096 grid64 L2^2 seed=rank gamma 2^5->2^16 to 1e-6",
+                   "n": n, "gamma_i": WORKLOAD["gamma_i"], "gamma_f": WORKLOAD["gamma_f"],
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "flushed between steps (512 MB write); C and P are 134 MB > L2",
+                   "stages": len(sols[0].iterations),
+                   "cg_iters": sum(i.stats.cg_iters for i in sols[0].iterations),
+                   "true_marginal_err": errs[0]},
+        "e2e": {"value": e2e / 1e3 / world, "unit": "s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches / max(args.steps, 1),
+        "roofline": {"bound": "hbm", "kernel": "k_coop (persistent CG/Newton)",
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "peak_source": hbm_src,
+                     "traffic": traffic,
+                     "alg_bytes_per_launch": alg_bytes / max(len(coop), 1),
+                     "launches": len(coop), "kernel_ms_total": coop_ms,
+                     "kernel_share_of_step": coop_ms / sum(step_ms)},
+        "clocks": clocks.summary(),
+        "per_step_ms": step_ms,
+        "e2e_per_step_ms": e2e_ms,
+        "calls_per_step": {k: v / args.steps for k, v in calls.items()},
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(host_prob, budget_s=args.cpu_budget)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm: the oracle port on the host cores
+# ---------------------------------------------------------------------------
+def cpu_baseline(prob, budget_s=15.0):
+    """Bounded kernel-mix sample of the reference's CPU path (oracle port),
+    scaled by the reference's call counts for this solve."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
+    from oracle import otn_oracle as orc
+
+    with open(CALLMIX) as fh:
+        mix = json.load(fh)
+    calls = mix["calls"]
+    n = prob.n
+    tally = orc.Tally()
+    gamma = WORKLOAD["gamma_f"] / 8.0
+    K = -gamma * prob.C
+    rng = np.random.default_rng(0)
+    u = np.log(prob.r) + 0.01 * rng.standard_normal(n)
+    v = np.log(prob.c) + 0.01 * rng.standard_normal(n)
+    st = orc.Dual(prob.C, gamma, u, v, prob.r, prob.c, tally)
+    P = orc.tiled_plan(K, u, v)
+    x = rng.standard_normal(n)
+    w = 1.0 / np.exp(st.log_c)
+
+    def timeit(fn, reps):
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        return (time.perf_counter() - t0) / reps
+
+    scale = budget_s / 15.0
+    per = {
+        "lse": timeit(lambda: orc.tiled_row_lse(K, u, v), max(2, int(12 * scale))),
+        "plan": timeit(lambda: orc.tiled_plan(K, u, v, out=P), max(1, int(5 * scale))),
+        "sqmv": timeit(lambda: orc.tiled_square_mv(P, w), max(1, int(5 * scale))),
+        "mv": timeit(lambda: orc.mv(P, x, tally), max(10, int(400 * scale))),
+        "rmv": timeit(lambda: orc.rmv(P, x, tally), max(10, int(400 * scale))),
+        "round": timeit(lambda: orc.round_to_polytope(P, prob.r, prob.c, tally), 1),
+    }
+    est = sum(calls.get(k, 0) * per[k] for k in per)
+    return {"value": est, "unit": "s", "cores": os.cpu_count(), "kind": "port",
+            "sample": ("oracle port (bit-exact to the reference), OpenBLAS with all host "
+                       "threads: per-call times of each dense primitive on this n=4096 "
+                       "problem, scaled by the reference's call counts for the D2 L2^2 s0 "
+                       f"solve {calls}"),
+            "per_call_s": per,
+            "reference_full_solve_s_build_container": mix.get("oracle_wall_s")}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path (the oracle port) on the host."""
+    from paper_2504_02067_b200 import problems
+    prob = problems.workload(WORKLOAD["spec"].format(seed=0))
+    budget = max(2.0, min(args.cpu_budget, 8.0))
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(prob, budget_s=2.0)
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(prob, budget_s=budget))
+    v = statistics.mean(x["value"] for x in vals)
+    cb = dict(vals[-1])
+    cb["value"] = v
+    return {
+        "metric": METRIC, "value": v, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded 64x64 grid cost + smooth-random marginals)",
+        "config": {"workload": "D2 n=4096 grid64 L2^2 seed=0 gamma 2^5->2^16 to 1e-6",
+                   "n": prob.n},
+        "impl": "reference",
+        "cpu_baseline": cb,
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+_PG = None
+
+
+def init_dist(args):
+    global _PG
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and args.impl != "reference":
+        import torch
+        import torch.distributed as dist
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        if backend == "nccl":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group(backend)
+        _PG = dist
+    return rank, world
+
+
+def barrier(world):
+    if world > 1 and _PG is not None:
+        _PG.barrier()
+
+
+def max_over_ranks(x, world):
+    if world > 1 and _PG is not None:
+        import torch
+        t = torch.tensor([x], dtype=torch.float64,
+                         device="cuda" if _PG.get_backend() == "nccl" else "cpu")
+        _PG.all_reduce(t, op=_PG.ReduceOp.MAX)
+        return float(t.item())
+    return x
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    rank, world = init_dist(args)
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        out = run_reference(args, rank, world)
+    else:
+        out = run_ours(args, rank, world)
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1 and _PG is not None:
+        _PG.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -117,15 +117,24 @@ int otn_trial_cols(otn_ctx* ctx, const double* C, int symmetric, double neg_gamm
                    double alpha, double* out, double* host_mass);
 
 /* ---- plan (K4 + K5) ------------------------------------------------------ */
-/* P_ij = exp((neg_gamma*C_ij + v_j) + u_i).  If icP != NULL also
- * mu_i = (sum_j P_ij^2 icP_j) / rP_i (the Jacobi diagonal, K5 fused).
- * Overflow (an exponent > 700) sets a device flag that the next otn_newton /
- * otn_pcg reports as OTN_ST_PLAN_OVERFLOW; when host_overflow != NULL the call
- * synchronizes and returns the flag.  Replaces _kernels.py:45-61
+/* A plan is the pair (P, seg_mask).  seg_mask (nullable = dense) holds one bit
+ * per 64-column (512-byte) row segment, set iff the segment has a nonzero:
+ * n rows x OTN_MASK_WORDS(ld) uint64 words, bit s%64 of word s/64 for segment
+ * s.  The Hessian-vector kernels skip all-zero segments (exp underflow makes
+ * most of the plan exactly 0 at weak regularization); skipped terms are exact
+ * zeros, so results are identical to the dense computation.                 */
+#define OTN_MASK_WORDS(ld) (((ld) + 4095) / 4096)
+/* P_ij = exp((neg_gamma*C_ij + v_j) + u_i), and seg_mask if non-NULL.  If
+ * icP != NULL also mu_i = (sum_j P_ij^2 icP_j) / rP_i (the Jacobi diagonal,
+ * K5 fused).  Overflow (an exponent > 700) sets a device flag that the next
+ * otn_newton reports as OTN_ST_PLAN_OVERFLOW; when host_overflow != NULL the
+ * call synchronizes and returns the flag.  Replaces _kernels.py:45-61
  * materialize_plan and newton.py:107-112 diag_prc / _kernels.py:64-74.     */
 int otn_materialize(otn_ctx* ctx, const double* C, double neg_gamma, const double* u,
                     const double* v, double* P, const double* icP, const double* rP,
-                    double* mu, int* host_overflow);
+                    double* mu, int* host_overflow, uint64_t* seg_mask);
+/* seg_mask of an externally supplied plan. */
+int otn_plan_mask(otn_ctx* ctx, const double* P, uint64_t* seg_mask);
 /* rP = exp(log_rP), cP = exp(log_cP), icP = 1/cP; nonpositive sums set the
  * OTN_ST_NONPOSITIVE_SUMS flag (DiscountedSystem.__init__, newton.py:72-90). */
 int otn_system_prep(otn_ctx* ctx, const double* log_rP, const double* log_cP, double* rP,
@@ -134,28 +143,38 @@ int otn_system_prep(otn_ctx* ctx, const double* log_rP, const double* log_cP, do
 int otn_square_matvec(otn_ctx* ctx, const double* P, const double* w, double* out);
 
 /* ---- Hessian-vector products (K6, K7) ------------------------------------ */
-int otn_matvec(otn_ctx* ctx, const double* P, const double* x, double* out);   /* newton.py:43-48  */
-int otn_rmatvec(otn_ctx* ctx, const double* P, const double* x, double* out);  /* newton.py:51-56  */
+int otn_matvec(otn_ctx* ctx, const double* P, const uint64_t* seg_mask, const double* x,
+               double* out);                                      /* newton.py:43-48  */
+int otn_rmatvec(otn_ctx* ctx, const double* P, const uint64_t* seg_mask, const double* x,
+                double* out);                                     /* newton.py:51-56  */
 /* out = rP*d - rho*P((P^T d)/cP)   (newton.py:100-105) */
-int otn_apply_F(otn_ctx* ctx, const double* P, const double* rP, const double* cP, double rho,
-                const double* d, double* out);
+int otn_apply_F(otn_ctx* ctx, const double* P, const uint64_t* seg_mask, const double* rP,
+                const double* cP, double rho, const double* d, double* out);
 /* out = (P^T d)/cP   (newton.py:96-98) */
-int otn_apply_pc(otn_ctx* ctx, const double* P, const double* cP, const double* d, double* out);
+int otn_apply_pc(otn_ctx* ctx, const double* P, const uint64_t* seg_mask, const double* cP,
+                 const double* d, double* out);
 
 /* ---- device-resident solvers (K8 + the CG / Newton loops) ----------------- */
 /* Jacobi-PCG on F(rho) x = b to L1 recurrence residual <= tol, x in/out
  * (has_x0 = 0: start from zero).  One persistent cooperative launch, no host
  * round trip per iteration.  Replaces newton.py:123-172 pcg_solve.          */
-int otn_pcg(otn_ctx* ctx, const double* P, const double* rP, const double* cP, const double* mu,
-            double rho, const double* b, double tol, double* x, int has_x0, int64_t max_iters,
-            otn_solve_result* host_res);
+int otn_pcg(otn_ctx* ctx, const double* P, const uint64_t* seg_mask, const double* rP,
+            const double* cP, const double* mu, double rho, const double* b, double tol,
+            double* x, int has_x0, int64_t max_iters, otn_solve_result* host_res);
 /* Annealed truncated-Newton direction (newton.py:175-210) for gradient g,
  * forcing eta, starting discount rho0; writes d_u and, if d_v != NULL, the
  * back-substitution d_v = -(P^T d_u)/cP plus the slope -(g.d_u)
  * (projector.py:196-205).  One persistent cooperative launch.               */
-int otn_newton(otn_ctx* ctx, const double* P, const double* rP, const double* cP,
-               const double* mu, const double* g, double eta, double rho0, int zero_init,
-               int64_t max_iters, double* d_u, double* d_v, otn_solve_result* host_res);
+int otn_newton(otn_ctx* ctx, const double* P, const uint64_t* seg_mask, const double* rP,
+               const double* cP, const double* mu, const double* g, double eta, double rho0,
+               int zero_init, int64_t max_iters, double* d_u, double* d_v,
+               otn_solve_result* host_res);
+
+/* Diagnostic: run building block `what` of the persistent solver `reps` times
+ * in one launch (0 grid barrier, 1 grid reduction, 2 column-partial pass,
+ * 3 row pass, 4 P^T x with its reductions, 5 full HVP).  Tooling only.     */
+int otn_probe(otn_ctx* ctx, const double* P, const uint64_t* seg_mask, const double* cP,
+              const double* rP, const double* x, double* out, int what, int64_t reps);
 
 /* ---- projector / driver vector work ------------------------------------- */
 int otn_vec(otn_ctx* ctx, int op, double s, const double* a, const double* b, const double* c,

@@ -57,6 +57,14 @@ class OracleFailure(Exception):
         self.diag = dict(diag or {})
 
 
+# Primitive call counter (bench.py's CPU-baseline kernel mix; not in the reference).
+CALLS = {}
+
+
+def _hit(name):
+    CALLS[name] = CALLS.get(name, 0) + 1
+
+
 # ---------------------------------------------------------------------------
 # operation tally (restates opcount.py:36-66; categories at the same sites)
 # ---------------------------------------------------------------------------
@@ -95,6 +103,7 @@ def tiled_row_lse(K, outer, inner):
     Per-row shift by the row max, numpy pairwise sum of the shifted exps over
     the whole row; tiled in 256-row slabs exactly like the reference.
     """
+    _hit("lse")
     rows = K.shape[0]
     res = np.empty(rows)
     scratch = np.empty((min(TILE_ROWS, rows), K.shape[1]))
@@ -115,6 +124,7 @@ def tiled_row_lse(K, outer, inner):
 
 def tiled_plan(K, u, v, out=None):
     """exp((K + v) + u) with the >700 overflow rejection.  (_kernels.py:45-61)"""
+    _hit("plan")
     rows, cols = K.shape
     out = np.empty((rows, cols)) if out is None else out
     for a in range(0, rows, TILE_ROWS):
@@ -131,6 +141,7 @@ def tiled_plan(K, u, v, out=None):
 
 def tiled_square_mv(P, w):
     """(P*P) @ w, one dgemv per 256-row slab.  (_kernels.py:64-74)"""
+    _hit("sqmv")
     rows = P.shape[0]
     res = np.empty(rows)
     scratch = np.empty((min(TILE_ROWS, rows), P.shape[1]))
@@ -144,12 +155,14 @@ def tiled_square_mv(P, w):
 
 def mv(P, x, tally):
     """P @ x (BLAS dgemv-N).  (newton.py:43-48)"""
+    _hit("mv")
     tally.bump(1)
     return P @ x
 
 
 def rmv(P, x, tally):
     """P.T @ x (BLAS dgemv-T).  (newton.py:51-56)"""
+    _hit("rmv")
     tally.bump(1)
     return P.T @ x
 
@@ -578,6 +591,7 @@ def extrapolate(z, zp, g_next, g, g_prev):  # driver.py:170-175
 
 
 def round_to_polytope(P, r, c, tally):  # driver.py:178-208
+    _hit("round")
     if P.min() < 0.0:
         raise OracleFailure("DomainError", "negative plan")
     if not P.sum() > 0.0:

@@ -46,6 +46,44 @@ def vptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+# Kernel launches issued by each C-ABI entry point (for the bench's
+# gpu_launches claim).  otn_lse_cols / otn_rebalance_cols / otn_trial_cols launch
+# one kernel for symmetric costs and two otherwise; trial adds the mass reduce.
+LAUNCHES = {
+    "otn_lse_rows": 1, "otn_lse_cols": 2, "otn_rebalance_cols": 2, "otn_trial_cols": 3,
+    "otn_materialize": 1, "otn_plan_mask": 1, "otn_system_prep": 1, "otn_square_matvec": 1, "otn_matvec": 1,
+    "otn_rmatvec": 1, "otn_apply_F": 1, "otn_apply_pc": 1, "otn_pcg": 1, "otn_newton": 1,
+    "otn_vec": 1, "otn_reduce": 1, "otn_round_plan": 10, "otn_probe": 1,
+}
+
+
+class Telemetry:
+    """Host-side counters for the bench: kernel launches, host<->device bytes,
+    and (when enabled) CUDA-event timing of the persistent solver launches."""
+
+    def __init__(self):
+        self.reset()
+        self.time_coop = False
+
+    def reset(self):
+        self.launches = 0
+        self.calls = {}
+        self.h2d = 0
+        self.d2h = 0
+        self.coop = []        # (start_event, end_event, hvps, n)
+
+    def count(self, name, sym=False):
+        k = LAUNCHES.get(name, 0)
+        if sym and name in ("otn_lse_cols", "otn_rebalance_cols", "otn_trial_cols"):
+            k -= 1
+        self.launches += k
+        self.calls[name] = self.calls.get(name, 0) + 1
+
+
+TELEMETRY = Telemetry()
+_SYM_CALLS = ("otn_lse_cols", "otn_rebalance_cols", "otn_trial_cols")
+
+
 def is_tensor(x):
     return type(x).__module__.startswith("torch") and hasattr(x, "data_ptr")
 
@@ -111,20 +149,28 @@ class Context:
         if is_tensor(values):
             buf[: self.n].copy_(values.reshape(-1)[: self.n].to(dtype=t.float64), non_blocking=True)
         else:
-            arr = np.ascontiguousarray(np.broadcast_to(np.asarray(values, dtype=np.float64),
-                                                       (self.n,)))
+            arr = np.array(np.broadcast_to(np.asarray(values, dtype=np.float64), (self.n,)))
             buf[: self.n].copy_(t.from_numpy(arr), non_blocking=False)
+            TELEMETRY.h2d += arr.nbytes
         return buf
 
     def download(self, buf):
-        return buf[: self.n].detach().cpu().numpy().copy()
+        out = buf[: self.n].detach().cpu().numpy().copy()
+        TELEMETRY.d2h += out.nbytes
+        return out
 
     def mat(self):
         t = torch()
         return t.zeros((self.n, self.ld), dtype=t.float64, device=self.device)
 
+    def seg_mask(self):
+        """Plan segment-occupancy mask (OTN_MASK_WORDS(ld) uint64 words per row)."""
+        t = torch()
+        return t.zeros((self.n, (self.ld + 4095) // 4096), dtype=t.int64, device=self.device)
+
     # ---- thin call helpers -----------------------------------------------
     def call(self, name, *args):
+        TELEMETRY.count(name, sym=bool(args[1]) if name in _SYM_CALLS else False)
         rc = getattr(self.lib, name)(self.h, *args)
         return _lib.check(rc, name)
 
@@ -148,6 +194,7 @@ class DeviceCost:
                 self.C[:, : self.n].copy_(C)
         else:
             host = t.from_numpy(np.ascontiguousarray(C, dtype=np.float64))
+            TELEMETRY.h2d += host.numel() * 8
             if ld == self.n:
                 self.C = host.to(device, non_blocking=False)
             else:

@@ -71,16 +71,18 @@ SIGNATURES = {
     "otn_lse_cols": [_P, _P, _I, _D, _P, _P, _P],
     "otn_rebalance_cols": [_P, _P, _I, _D, _P, _P, _P],
     "otn_trial_cols": [_P, _P, _I, _D, _P, _P, _P, _P, _D, _P, _DP],
-    "otn_materialize": [_P, _P, _D, _P, _P, _P, _P, _P, _P, _IP],
+    "otn_materialize": [_P, _P, _D, _P, _P, _P, _P, _P, _P, _IP, _P],
+    "otn_plan_mask": [_P, _P, _P],
     "otn_system_prep": [_P, _P, _P, _P, _P, _P, _IP],
     "otn_square_matvec": [_P, _P, _P, _P],
-    "otn_matvec": [_P, _P, _P, _P],
-    "otn_rmatvec": [_P, _P, _P, _P],
-    "otn_apply_F": [_P, _P, _P, _P, _D, _P, _P],
-    "otn_apply_pc": [_P, _P, _P, _P, _P],
-    "otn_pcg": [_P, _P, _P, _P, _P, _D, _P, _D, _P, _I, _I64, ctypes.POINTER(SolveResult)],
-    "otn_newton": [_P, _P, _P, _P, _P, _P, _D, _D, _I, _I64, _P, _P,
+    "otn_matvec": [_P, _P, _P, _P, _P],
+    "otn_rmatvec": [_P, _P, _P, _P, _P],
+    "otn_apply_F": [_P, _P, _P, _P, _P, _D, _P, _P],
+    "otn_apply_pc": [_P, _P, _P, _P, _P, _P],
+    "otn_pcg": [_P, _P, _P, _P, _P, _P, _D, _P, _D, _P, _I, _I64, ctypes.POINTER(SolveResult)],
+    "otn_newton": [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I, _I64, _P, _P,
                    ctypes.POINTER(SolveResult)],
+    "otn_probe": [_P, _P, _P, _P, _P, _P, _P, _I, _I64],
     "otn_vec": [_P, _I, _D, _P, _P, _P, _P, _P],
     "otn_reduce": [_P, _I, _P, _P, _P, _P, _DP, _IP],
     "otn_round_plan": [_P, _P, _P, _P, _P, _DP, _IP],

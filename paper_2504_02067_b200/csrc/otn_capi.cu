@@ -103,6 +103,16 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
     return fail(OTN_ERR_CUDA, "otn_create: persistent solver does not fit on an SM", e);
   }
   x->coop_blocks = x->num_sms;   // one CTA per SM (co-residency guaranteed)
+  {
+    // the persistent solver stages each CTA's (row, tile) spans in shared memory
+    const int64_t rows = (n + x->coop_blocks - 1) / x->coop_blocks;
+    const int64_t tiles = (ld + 4095) / 4096;
+    if (rows * tiles > 8192 || tiles > 64) {
+      delete x;
+      return fail(OTN_ERR_ARG, "otn_create: n too large for the stored-plan solver "
+                               "(rows per SM x 4096-column tiles must be <= 8192)");
+    }
+  }
   // column-reduction slabs: ~4 CTAs per SM over ld/64 column tiles
   {
     const int64_t tiles = (ld + otn::kColTile - 1) / otn::kColTile;
@@ -242,11 +252,12 @@ int otn_trial_cols(otn_ctx* x, const double* C, int sym, double ng, const double
 
 // ---- plan ----------------------------------------------------------------
 int otn_materialize(otn_ctx* x, const double* C, double ng, const double* u, const double* v,
-                    double* P, const double* icP, const double* rP, double* mu, int* host_overflow) {
+                    double* P, const double* icP, const double* rP, double* mu, int* host_overflow,
+                    uint64_t* seg_mask) {
   OTN_REQUIRE(x && C && u && v && P, "otn_materialize: NULL argument");
   OTN_REQUIRE(!icP || (rP && mu), "otn_materialize: icP needs rP and mu");
   OTN_CUDA(cudaMemsetAsync(x->flags + 0, 0, sizeof(int), x->stream), "otn_materialize: flag");
-  OTN_CUDA(otn::launch_materialize(x, C, ng, u, v, P, icP, rP, mu, x->flags + 0),
+  OTN_CUDA(otn::launch_materialize(x, C, ng, u, v, P, icP, rP, mu, x->flags + 0, seg_mask),
            "otn_materialize");
   if (host_overflow) {
     int rc = sync_copy(x, x->h_flags, x->flags, sizeof(int), "otn_materialize: flag copy");
@@ -254,6 +265,12 @@ int otn_materialize(otn_ctx* x, const double* C, double ng, const double* u, con
     *host_overflow = x->h_flags[0];
     if (x->h_flags[0]) return OTN_ST_PLAN_OVERFLOW;
   }
+  return OTN_OK;
+}
+
+int otn_plan_mask(otn_ctx* x, const double* P, uint64_t* seg_mask) {
+  OTN_REQUIRE(x && P && seg_mask, "otn_plan_mask: NULL argument");
+  OTN_CUDA(otn::launch_plan_mask(x, P, seg_mask), "otn_plan_mask");
   return OTN_OK;
 }
 
@@ -278,9 +295,17 @@ int otn_square_matvec(otn_ctx* x, const double* P, const double* w, double* out)
 }
 
 // ---- HVP seam operators (single cooperative launch each) -------------------
-static int coop_op(otn_ctx* x, int mode, const double* P, const double* rP, const double* cP,
-                   double rho, const double* xin, double* out, const char* what) {
+static otn::CoopArgs plan_args(otn_ctx* x, const double* P, const uint64_t* seg_mask) {
   otn::CoopArgs a = base_args(x, P);
+  a.mask = seg_mask;
+  a.mw = (x->ld + otn::kSegWordCols - 1) / otn::kSegWordCols;
+  return a;
+}
+
+static int coop_op(otn_ctx* x, int mode, const double* P, const uint64_t* seg_mask,
+                   const double* rP, const double* cP, double rho, const double* xin, double* out,
+                   const char* what) {
+  otn::CoopArgs a = plan_args(x, P, seg_mask);
   a.mode = mode;
   a.rP = rP;
   a.cP = cP;
@@ -291,34 +316,35 @@ static int coop_op(otn_ctx* x, int mode, const double* P, const double* rP, cons
   return OTN_OK;
 }
 
-int otn_matvec(otn_ctx* x, const double* P, const double* v, double* out) {
+int otn_matvec(otn_ctx* x, const double* P, const uint64_t* m, const double* v, double* out) {
   OTN_REQUIRE(x && P && v && out, "otn_matvec: NULL argument");
-  return coop_op(x, otn::kModeMatvec, P, nullptr, nullptr, 0.0, v, out, "otn_matvec");
+  return coop_op(x, otn::kModeMatvec, P, m, nullptr, nullptr, 0.0, v, out, "otn_matvec");
 }
 
-int otn_rmatvec(otn_ctx* x, const double* P, const double* v, double* out) {
+int otn_rmatvec(otn_ctx* x, const double* P, const uint64_t* m, const double* v, double* out) {
   OTN_REQUIRE(x && P && v && out, "otn_rmatvec: NULL argument");
-  return coop_op(x, otn::kModeRmatvec, P, nullptr, nullptr, 0.0, v, out, "otn_rmatvec");
+  return coop_op(x, otn::kModeRmatvec, P, m, nullptr, nullptr, 0.0, v, out, "otn_rmatvec");
 }
 
-int otn_apply_F(otn_ctx* x, const double* P, const double* rP, const double* cP, double rho,
-                const double* d, double* out) {
+int otn_apply_F(otn_ctx* x, const double* P, const uint64_t* m, const double* rP,
+                const double* cP, double rho, const double* d, double* out) {
   OTN_REQUIRE(x && P && rP && cP && d && out, "otn_apply_F: NULL argument");
-  return coop_op(x, otn::kModeHvp, P, rP, cP, rho, d, out, "otn_apply_F");
+  return coop_op(x, otn::kModeHvp, P, m, rP, cP, rho, d, out, "otn_apply_F");
 }
 
-int otn_apply_pc(otn_ctx* x, const double* P, const double* cP, const double* d, double* out) {
+int otn_apply_pc(otn_ctx* x, const double* P, const uint64_t* m, const double* cP,
+                 const double* d, double* out) {
   OTN_REQUIRE(x && P && cP && d && out, "otn_apply_pc: NULL argument");
-  return coop_op(x, otn::kModePc, P, nullptr, cP, 0.0, d, out, "otn_apply_pc");
+  return coop_op(x, otn::kModePc, P, m, nullptr, cP, 0.0, d, out, "otn_apply_pc");
 }
 
 // ---- solvers ---------------------------------------------------------------
-int otn_pcg(otn_ctx* x, const double* P, const double* rP, const double* cP, const double* mu,
-            double rho, const double* b, double tol, double* xv, int has_x0, int64_t max_iters,
-            otn_solve_result* host_res) {
+int otn_pcg(otn_ctx* x, const double* P, const uint64_t* m, const double* rP, const double* cP,
+            const double* mu, double rho, const double* b, double tol, double* xv, int has_x0,
+            int64_t max_iters, otn_solve_result* host_res) {
   OTN_REQUIRE(x && P && rP && cP && mu && b && xv, "otn_pcg: NULL argument");
   OTN_REQUIRE(max_iters >= 0, "otn_pcg: max_iters < 0");
-  otn::CoopArgs a = base_args(x, P);
+  otn::CoopArgs a = plan_args(x, P, m);
   a.mode = otn::kModePcg;
   a.rP = rP;
   a.cP = cP;
@@ -333,12 +359,12 @@ int otn_pcg(otn_ctx* x, const double* P, const double* rP, const double* cP, con
   return finish_solve(x, host_res, "otn_pcg: result");
 }
 
-int otn_newton(otn_ctx* x, const double* P, const double* rP, const double* cP, const double* mu,
-               const double* g, double eta, double rho0, int zero_init, int64_t max_iters,
-               double* d_u, double* d_v, otn_solve_result* host_res) {
+int otn_newton(otn_ctx* x, const double* P, const uint64_t* m, const double* rP, const double* cP,
+               const double* mu, const double* g, double eta, double rho0, int zero_init,
+               int64_t max_iters, double* d_u, double* d_v, otn_solve_result* host_res) {
   OTN_REQUIRE(x && P && rP && cP && mu && g && d_u, "otn_newton: NULL argument");
   OTN_REQUIRE(max_iters >= 0, "otn_newton: max_iters < 0");
-  otn::CoopArgs a = base_args(x, P);
+  otn::CoopArgs a = plan_args(x, P, m);
   a.mode = otn::kModeNewton;
   a.rP = rP;
   a.cP = cP;
@@ -353,6 +379,21 @@ int otn_newton(otn_ctx* x, const double* P, const double* rP, const double* cP, 
   a.pre_flags = x->flags;
   OTN_CUDA(otn::launch_coop(x, a), "otn_newton");
   return finish_solve(x, host_res, "otn_newton: result");
+}
+
+int otn_probe(otn_ctx* x, const double* P, const uint64_t* m, const double* cP, const double* rP,
+              const double* xin, double* out, int what, int64_t reps) {
+  OTN_REQUIRE(x && P && cP && rP && xin && out, "otn_probe: NULL argument");
+  otn::CoopArgs a = plan_args(x, P, m);
+  a.mode = otn::kModeProbe;
+  a.cP = cP;
+  a.rP = rP;
+  a.xin = xin;
+  a.d = out;
+  a.has_x0 = what;
+  a.max_iters = reps;
+  OTN_CUDA(otn::launch_coop(x, a), "otn_probe");
+  return OTN_OK;
 }
 
 // ---- vector work -----------------------------------------------------------

@@ -32,19 +32,26 @@ constexpr int NW = NT / 32;         // warps per CTA
 constexpr int CH = 4;               // 16-byte chunks per thread per tile
 constexpr int TILE = NT * 2 * CH;   // 4096 columns
 constexpr int RB = 4;               // rows per phase-B group
+constexpr int kRows = 64;           // rows staged per chunk in phases A / B
 constexpr int kRefresh = 50;        // newton.py:38 TRUE_RESIDUAL_REFRESH
+constexpr int kMaxG = 256;          // grid-reduction fan-in handled in one pass
 
 struct Smem {
   double red[4][33];
   double gres[4];
   double a2[NW][33];
-  double bpart[2][NW][RB];
+  double xs[kRows];                 // phase A: this chunk's x_i
+  double bp[NW][kRows];             // phase B: per-warp partial row dots
 };
 
 __device__ __forceinline__ double2 ldcg2(const double* p) {
   return __ldcg(reinterpret_cast<const double2*>(p));
 }
 
+// Deterministic grid-wide sum of K values: fixed warp / block / grid trees.
+// Value k is reduced by warp k (in parallel); one grid barrier; one L2 round
+// trip for the G partials.  Slots rotate so a fast CTA never overwrites
+// partials a slow CTA is still reading.
 template <int K>
 __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&v)[K], double* red,
                                             int& slot, Smem& sh) {
@@ -52,30 +59,31 @@ __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&v)[K]
   const int G = gridDim.x;
 #pragma unroll
   for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
-  __syncthreads();
   if (lane == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) sh.red[k][warp] = v[k];
   }
   __syncthreads();
-  if (warp == 0) {
-    double* dst = red + (int64_t(slot) * G + blockIdx.x) * kRedWidth;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const double t = warp_sum(lane < NW ? sh.red[k][lane] : 0.0);
-      if (lane == 0) dst[k] = t;
-    }
+  if (warp < K) {
+    const double t = warp_sum(lane < NW ? sh.red[warp][lane] : 0.0);
+    if (lane == 0) red[(int64_t(slot) * G + blockIdx.x) * kRedWidth + warp] = t;
   }
   grid.sync();
-  if (warp == 0) {
-    const double* src = red + int64_t(slot) * G * kRedWidth;
+  if (warp < K) {
+    const double* src = red + int64_t(slot) * G * kRedWidth + warp;
+    double t = 0.0;
+    for (int b0 = 0; b0 < G; b0 += kMaxG) {
+      double part[kMaxG / 32];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double t = 0.0;
-      for (int b = lane; b < G; b += 32) t += __ldcg(src + int64_t(b) * kRedWidth + k);
-      t = warp_sum(t);
-      if (lane == 0) sh.gres[k] = t;
+      for (int m = 0; m < kMaxG / 32; ++m) {
+        const int b = b0 + lane + 32 * m;
+        part[m] = b < G ? __ldcg(src + int64_t(b) * kRedWidth) : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < kMaxG / 32; ++m) t += part[m];
     }
+    t = warp_sum(t);
+    if (lane == 0) sh.gres[warp] = t;
   }
   __syncthreads();
 #pragma unroll
@@ -83,55 +91,183 @@ __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&v)[K]
   slot ^= 1;
 }
 
-// Phase A: column partials of P^T x over this CTA's rows.
-__device__ __noinline__ void phase_a(const CoopArgs& a, const double* x, int64_t r0, int64_t r1, double* wrow) {
+// ---------------------------------------------------------------------------
+// Plan streaming: per-CTA column windows + per-thread cp.async rings.
+//
+// A work item is one row i of one 4096-column tile T of the plan; its span
+// [lo, hi) runs from the first to the last nonzero 64-column segment
+// (seg_mask: exp underflow makes most of the plan exactly 0 at weak
+// regularization; for pixel-grid costs a row's nonzero segments are one
+// contiguous run).  At kernel start each CTA stages the spans of its rows and
+// their union per tile — its column WINDOW — in shared memory.  Within a tile
+// thread t owns window columns {2t, 2t+1} + c*1024 (c < nch = ceil(W/1024)),
+// so for a sparse plan all threads work on the few nonzero columns instead of
+// most of them idling.  Each thread streams exactly its 16-byte chunks of each
+// row's span, kRingDepth-1 rows ahead, with cp.async (LDGSTS, L1-bypassing)
+// into its own ring slots and reads only what it copied: no barrier of any
+// kind inside a phase.  Chunks outside the span are exact zeros and are
+// neither loaded nor used: the results equal the dense computation bit for bit.
+// ---------------------------------------------------------------------------
+constexpr int kRingDepth = 5;                       // rows per thread ring
+constexpr int kSpanSmem = 8192;                     // (row, tile) spans staged per CTA (32 KB)
+constexpr int kMaxTiles = 64;                       // ld <= 262144
+__shared__ uint32_t s_span[kSpanSmem];              // lo | hi << 16, relative to the tile
+__shared__ int s_win_lo[kMaxTiles], s_win_hi[kMaxTiles];
+extern __shared__ __align__(128) double2 s_ring[];  // [kRingDepth][CH][NT] double2
+
+// Everything the streaming loops need, by value (registers, not the kernel's
+// parameter copy in local memory).
+struct PlanView {
+  const double* P;
+  const uint64_t* mask;     // global mask rows (nullptr = dense)
+  int64_t ld, mw;
+  int nt;                   // tiles
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ int ntiles_of(int64_t ld) { return int((ld + TILE - 1) / TILE); }
+
+// Span of global row i in tile ti straight from the global mask.
+__device__ __forceinline__ void mask_span(const PlanView& v, int64_t i, int ti, int& lo, int& hi) {
+  const int64_t T = int64_t(ti) * TILE;
+  const int width = int(v.ld - T < TILE ? v.ld - T : int64_t(TILE));
+  if (!v.mask) { lo = 0; hi = width; return; }
+  const uint64_t bits = __ldg(v.mask + i * v.mw + T / kSegWordCols);
+  if (!bits) { lo = hi = 0; return; }
+  lo = (__ffsll(static_cast<long long>(bits)) - 1) * kSegCols;
+  hi = min((64 - __clzll(static_cast<long long>(bits))) * kSegCols, width);
+}
+
+// Span of row r0 + il (il = row index within the CTA) in tile ti.
+__device__ __forceinline__ void get_span(const PlanView& v, int il, int ti, int& lo, int& hi) {
+  const uint32_t s = s_span[il * v.nt + ti];
+  lo = int(s & 0xffffu);
+  hi = int(s >> 16);
+}
+
+// col in [lo, hi) with one compare (lo <= hi): outside-span chunks and the
+// chunks past the window end (col >= uhi >= hi) both fail it.
+__device__ __forceinline__ bool in_span(int col, int lo, int hi) {
+  return unsigned(col - lo) < unsigned(hi - lo);
+}
+
+__device__ PlanView plan_view(const CoopArgs& a, int64_t r0, int64_t r1) {
+  PlanView v;
+  v.P = a.P;
+  v.mask = a.mask;
+  v.ld = a.ld;
+  v.mw = a.mw;
+  v.nt = ntiles_of(a.ld);
+  return v;
+}
+
+// Stage spans and windows; zero this CTA's column-partial row outside its
+// windows (phase A writes only inside them, A2 reads the whole row).
+__device__ void stage_layout(const CoopArgs& a, int64_t r0, int64_t r1, double* wrow) {
+  const PlanView v = plan_view(a, r0, r1);
   const int t = threadIdx.x;
-  for (int64_t tile = 0; tile < a.ld; tile += TILE) {
+  const int64_t items = (r1 - r0) * v.nt;
+  if (t < v.nt) { s_win_lo[t] = 1 << 30; s_win_hi[t] = 0; }
+  __syncthreads();
+  for (int64_t k = t; k < items; k += NT) {
+    const int ti = int(k % v.nt);
+    int lo, hi;
+    mask_span(v, r0 + k / v.nt, ti, lo, hi);
+    s_span[k] = uint32_t(lo) | (uint32_t(hi) << 16);
+    if (lo < hi) {
+      atomicMin(&s_win_lo[ti], lo);
+      atomicMax(&s_win_hi[ti], hi);
+    }
+  }
+  __syncthreads();
+  if (t < v.nt && s_win_lo[t] >= s_win_hi[t]) s_win_lo[t] = s_win_hi[t] = 0;
+  __syncthreads();
+  for (int64_t j = 2 * int64_t(t); j < a.ld; j += 2 * NT) {
+    const int ti = int(j / TILE), rel = int(j - int64_t(ti) * TILE);
+    if (rel < s_win_lo[ti] || rel >= s_win_hi[ti])
+      *reinterpret_cast<double2*>(wrow + j) = make_double2(0.0, 0.0);
+  }
+}
+
+// Issue this thread's chunks of row il into ring slot `slot` (smem byte
+// address `dst`), then commit one group (possibly empty).
+__device__ __forceinline__ void ring_fill(const PlanView& v, const double* src_row, int il, int ti,
+                                          int col0, uint32_t dst) {
+  int lo, hi;
+  get_span(v, il, ti, lo, hi);
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int col = col0 + c * NT * 2;
+    if (in_span(col, lo, hi)) cp_async16(dst + c * NT * 16, src_row + col);
+  }
+  cp_commit();
+}
+
+// Phase A: column partials of P^T x over this CTA's rows (ascending).
+__device__ __noinline__ void phase_a(const PlanView v, const double* x, int64_t r0, int64_t r1,
+                                     double* wrow, Smem& sh) {
+  const int t = threadIdx.x;
+  const uint32_t ring0 = smem_u32(s_ring) + 16u * t;
+  constexpr uint32_t kSlotBytes = CH * NT * 16;
+  const int rows = int(r1 - r0);
+  for (int ti = 0; ti < v.nt; ++ti) {
+    const int64_t T = int64_t(ti) * TILE;
+    const int ulo = s_win_lo[ti], W = s_win_hi[ti] - ulo;
+    if (W <= 0) continue;
+    const int col0 = ulo + 2 * t;
     double2 acc[CH];
-    bool ok[CH];
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      acc[c] = make_double2(0.0, 0.0);
-      ok[c] = tile + c * NT * 2 + 2 * t < a.ld;
-    }
-    const double* base = a.P + tile + 2 * t;
-    int64_t i = r0;
-    for (; i + 1 < r1; i += 2) {
-      const double x0 = x[i], x1 = x[i + 1];
-      const double* p0 = base + i * a.ld;
-      double2 v0[CH], v1[CH];
+    for (int c = 0; c < CH; ++c) acc[c] = make_double2(0.0, 0.0);
+    for (int c0 = 0; c0 < rows; c0 += kRows) {
+      const int m = min(rows - c0, kRows);
+      __syncthreads();
+      for (int k = t; k < m; k += NT) sh.xs[k] = x[r0 + c0 + k];
+      __syncthreads();
+      const double* fill_row = v.P + (r0 + c0) * v.ld + T;   // next row to stream
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        if (ok[c]) {
-          v0[c] = ld_stream2(p0 + c * NT * 2);
-          v1[c] = ld_stream2(p0 + a.ld + c * NT * 2);
-        }
+      for (int d = 0; d < kRingDepth - 1; ++d) {
+        if (d < m) ring_fill(v, fill_row, c0 + d, ti, col0, ring0 + d * kSlotBytes);
+        else cp_commit();
+        fill_row += v.ld;
       }
+      int slot = 0;
+      uint32_t fdst = ring0 + (kRingDepth - 1) * kSlotBytes;
+      for (int q = 0; q < m; ++q) {
+        if (q + kRingDepth - 1 < m) ring_fill(v, fill_row, c0 + q + kRingDepth - 1, ti, col0, fdst);
+        else cp_commit();
+        fill_row += v.ld;
+        fdst = fdst == ring0 + (kRingDepth - 1) * kSlotBytes ? ring0 : fdst + kSlotBytes;
+        cp_wait<kRingDepth - 1>();
+        int lo, hi;
+        get_span(v, c0 + q, ti, lo, hi);
+        const double xi = sh.xs[q];
+        const double2* row = s_ring + slot * CH * NT + t;
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        if (ok[c]) {
-          acc[c].x = fma(v0[c].x, x0, acc[c].x);
-          acc[c].y = fma(v0[c].y, x0, acc[c].y);
-          acc[c].x = fma(v1[c].x, x1, acc[c].x);
-          acc[c].y = fma(v1[c].y, x1, acc[c].y);
+        for (int c = 0; c < CH; ++c) {
+          if (in_span(col0 + c * NT * 2, lo, hi)) {
+            const double2 pv = row[c * NT];
+            acc[c].x = fma(pv.x, xi, acc[c].x);
+            acc[c].y = fma(pv.y, xi, acc[c].y);
+          }
         }
-      }
-    }
-    if (i < r1) {
-      const double x0 = x[i];
-      const double* p0 = base + i * a.ld;
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        if (ok[c]) {
-          const double2 v = ld_stream2(p0 + c * NT * 2);
-          acc[c].x = fma(v.x, x0, acc[c].x);
-          acc[c].y = fma(v.y, x0, acc[c].y);
-        }
+        slot = slot + 1 == kRingDepth ? 0 : slot + 1;
       }
     }
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
-      if (ok[c]) *reinterpret_cast<double2*>(wrow + tile + c * NT * 2 + 2 * t) = acc[c];
+      const int rel = c * NT * 2 + 2 * t;
+      if (rel < W) *reinterpret_cast<double2*>(wrow + T + ulo + rel) = acc[c];
     }
   }
 }
@@ -146,7 +282,17 @@ __device__ __noinline__ void phase_a2(const CoopArgs& a, int kind, double* out, 
   for (int64_t s = blockIdx.x; s * 32 < a.ld; s += G) {
     const int64_t j = s * 32 + lane;
     double acc = 0.0;
-    for (int bp = warp; bp < G; bp += NW) acc += __ldcg(a.wpart + int64_t(bp) * a.ld + j);
+    // issue all of this warp's partial loads before summing (latency-bound otherwise)
+    for (int b0 = warp; b0 < G; b0 += NW * 16) {
+      double v[16];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        const int bp = b0 + m * NW;
+        v[m] = bp < G ? __ldcg(a.wpart + int64_t(bp) * a.ld + j) : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < 16; ++m) acc += v[m];
+    }
     sh.a2[warp][lane] = acc;
     __syncthreads();
     if (warp == 0) {
@@ -164,61 +310,107 @@ __device__ __noinline__ void phase_a2(const CoopArgs& a, int kind, double* out, 
   }
 }
 
-// Phase B: s_i = sum_j P_ij w_j for own rows (descending), into sv[i].
-__device__ __noinline__ void phase_b(const CoopArgs& a, const double* w, int64_t r0, int64_t r1, double* sv,
-                        Smem& sh) {
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  int buf = 0;
-  for (int64_t tile = 0; tile < a.ld; tile += TILE) {
-    double2 wv[CH];
-    bool ok[CH];
+// Sum eight per-lane values over the warp with a transpose-reduction (fixed
+// butterfly, 9 shuffles instead of 8 x 5): on return lane l holds the total of
+// value ((l>>4)&1)*4 + ((l>>3)&1)*2 + ((l>>2)&1).
+__device__ __forceinline__ double warp_reduce8(const double (&d)[8], int lane) {
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+  double w4[4], w2[2];
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      const int64_t j = tile + c * NT * 2 + 2 * t;
-      ok[c] = j < a.ld;
-      wv[c] = ok[c] ? ldcg2(w + j) : make_double2(0.0, 0.0);
-    }
-    const double* base = a.P + tile + 2 * t;
-    for (int64_t hi = r1; hi > r0; hi -= RB) {
-      double dot[RB];
-      double2 v[RB][CH];
-#pragma unroll
-      for (int k = 0; k < RB; ++k) {
-        dot[k] = 0.0;
-        const int64_t i = hi - 1 - k;
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          if (i >= r0 && ok[c]) v[k][c] = ld_stream2(base + i * a.ld + c * NT * 2);
-          else v[k][c] = make_double2(0.0, 0.0);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < RB; ++k) {
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          dot[k] = fma(v[k][c].x, wv[c].x, dot[k]);
-          dot[k] = fma(v[k][c].y, wv[c].y, dot[k]);
-        }
-        dot[k] = warp_sum(dot[k]);
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < RB; ++k) sh.bpart[buf][warp][k] = dot[k];
-      }
-      __syncthreads();
-      if (t < RB) {
-        const int64_t i = hi - 1 - t;
-        if (i >= r0) {
-          double tot = 0.0;
-#pragma unroll 8
-          for (int ww = 0; ww < NW; ++ww) tot += sh.bpart[buf][ww][t];
-          sv[i] = tile == 0 ? tot : sv[i] + tot;
-        }
-      }
-      buf ^= 1;
-    }
+  for (int k = 0; k < 4; ++k) {
+    const double keep = h16 ? d[k + 4] : d[k], give = h16 ? d[k] : d[k + 4];
+    w4[k] = keep + __shfl_xor_sync(0xffffffffu, give, 16);
   }
-  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double keep = h8 ? w4[k + 2] : w4[k], give = h8 ? w4[k] : w4[k + 2];
+    w2[k] = keep + __shfl_xor_sync(0xffffffffu, give, 8);
+  }
+  const double keep = h4 ? w2[1] : w2[0], give = h4 ? w2[0] : w2[1];
+  double s = keep + __shfl_xor_sync(0xffffffffu, give, 4);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  return s;
+}
+
+// Phase B: s_i = sum_j P_ij w_j for own rows (DESCENDING: the rows phase A
+// streamed last are the likeliest L2 hits), into sv[i].  Per-lane dots of 8
+// rows are combined by one transpose-reduction; per-warp partials accumulate in
+// shared memory; one fixed-order sum over warps per chunk.
+__device__ __noinline__ void phase_b(const PlanView v, const double* w, int64_t r0, int64_t r1,
+                                     double* sv, Smem& sh) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t ring0 = smem_u32(s_ring) + 16u * t;
+  constexpr uint32_t kSlotBytes = CH * NT * 16;
+  const int rows = int(r1 - r0);
+  const int row_of_lane = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  for (int e = rows; e > 0; e -= kRows) {          // chunk [e - m, e) of CTA rows
+    const int m = min(e, kRows), c0 = e - m;
+    for (int k = lane; k < m; k += 32) sh.bp[warp][k] = 0.0;
+    __syncwarp();
+    for (int ti = 0; ti < v.nt; ++ti) {
+      const int64_t T = int64_t(ti) * TILE;
+      const int ulo = s_win_lo[ti], W = s_win_hi[ti] - ulo;
+      if (W <= 0) continue;
+      const int col0 = ulo + 2 * t;
+      double2 wv[CH];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int rel = c * NT * 2 + 2 * t;
+        wv[c] = rel < W ? ldcg2(w + T + ulo + rel) : make_double2(0.0, 0.0);
+      }
+      const double* fill_row = v.P + (r0 + e - 1) * v.ld + T;
+#pragma unroll
+      for (int d = 0; d < kRingDepth - 1; ++d) {
+        if (d < m) ring_fill(v, fill_row, e - 1 - d, ti, col0, ring0 + d * kSlotBytes);
+        else cp_commit();
+        fill_row -= v.ld;
+      }
+      int slot = 0;
+      uint32_t fdst = ring0 + (kRingDepth - 1) * kSlotBytes;
+      double d8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) d8[k] = 0.0;
+      for (int q = 0; q < m; ++q) {
+        if (q + kRingDepth - 1 < m) ring_fill(v, fill_row, e - kRingDepth - q, ti, col0, fdst);
+        else cp_commit();
+        fill_row -= v.ld;
+        fdst = fdst == ring0 + (kRingDepth - 1) * kSlotBytes ? ring0 : fdst + kSlotBytes;
+        cp_wait<kRingDepth - 1>();
+        int lo, hi;
+        get_span(v, e - 1 - q, ti, lo, hi);
+        const double2* row = s_ring + slot * CH * NT + t;
+        double dot = 0.0;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          if (in_span(col0 + c * NT * 2, lo, hi)) {
+            const double2 pv = row[c * NT];
+            dot = fma(pv.x, wv[c].x, dot);
+            dot = fma(pv.y, wv[c].y, dot);
+          }
+        }
+        const int b = q & 7;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k == b) d8[k] = dot;
+        if (b == 7 || q == m - 1) {
+          const double s = warp_reduce8(d8, lane);
+          if ((lane & 3) == 0 && row_of_lane <= b) sh.bp[warp][e - 1 - (q - b + row_of_lane) - c0] += s;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) d8[k] = 0.0;
+        }
+        slot = slot + 1 == kRingDepth ? 0 : slot + 1;
+      }
+    }
+    __syncthreads();
+    if (t < m) {
+      double tot = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < NW; ++ww) tot += sh.bp[ww][t];
+      sv[r0 + c0 + t] = tot;
+    }
+    __syncthreads();
+  }
 }
 
 // q = F(rho) x on own rows (newton.py:100-105; matvecs skipped when rho == 0).
@@ -227,11 +419,11 @@ __device__ void hvp(cg::grid_group& grid, const CoopArgs& a, const double* x, do
   if (rho != 0.0) {
     ++nh;
     __syncthreads();
-    phase_a(a, x, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld);
+    phase_a(plan_view(a, r0, r1), x, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
     grid.sync();
     phase_a2(a, 0, a.wc, sh);
     grid.sync();
-    phase_b(a, a.wc, r0, r1, a.sv, sh);
+    phase_b(plan_view(a, r0, r1), a.wc, r0, r1, a.sv, sh);
   }
   for (int64_t i = r0 + threadIdx.x; i < r1; i += NT) {
     double o = __dmul_rn(__ldg(a.rP + i), x[i]);
@@ -328,6 +520,7 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
   int64_t nh = 0;
   DevResult res{};
   res.status = OTN_OK;
+  stage_layout(a, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld);
 
   if (a.pre_flags) {
     // [0]: plan overflow (materialize), [1]: nonpositive sums (system prep);
@@ -390,7 +583,7 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
     }
     if (res.status == OTN_OK && a.dv) {
       __syncthreads();
-      phase_a(a, a.d, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld);
+      phase_a(plan_view(a, r0, r1), a.d, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
       grid.sync();
       phase_a2(a, 1, a.dv, sh);
       double sl[1] = {0.0};
@@ -410,32 +603,63 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
   } else if (a.mode == kModeHvp) {
     hvp(grid, a, a.xin, a.rho, a.d, r0, r1, sh, nh);
   } else if (a.mode == kModePc || a.mode == kModeRmatvec) {
-    phase_a(a, a.xin, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld);
+    phase_a(plan_view(a, r0, r1), a.xin, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
     grid.sync();
     phase_a2(a, a.mode == kModePc ? 0 : 2, a.wc, sh);
     grid.sync();
     for (int64_t i = int64_t(blockIdx.x) * NT + threadIdx.x; i < a.n; i += int64_t(G) * NT)
       a.d[i] = __ldcg(a.wc + i);
+  } else if (a.mode == kModeProbe) {
+    // Diagnostic: repeat one building block max_iters times (bench tooling).
+    const int what = a.has_x0;
+    for (int64_t k = 0; k < a.max_iters; ++k) {
+      if (what == 0) {
+        grid.sync();
+      } else if (what == 1) {
+        double v[2] = {1.0, 2.0};
+        grid_reduce<2>(grid, v, a.red, slot, sh);
+      } else if (what == 2) {
+        phase_a(plan_view(a, r0, r1), a.xin, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
+        __syncthreads();
+      } else if (what == 3) {
+        phase_b(plan_view(a, r0, r1), a.xin, r0, r1, a.sv, sh);
+      } else if (what == 4) {
+        phase_a(plan_view(a, r0, r1), a.xin, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
+        grid.sync();
+        phase_a2(a, 0, a.wc, sh);
+        grid.sync();
+      } else {
+        hvp(grid, a, a.xin, 0.5, a.d, r0, r1, sh, nh);
+      }
+    }
   } else if (a.mode == kModeMatvec) {
     // stage x into the padded workspace vector (phase B reads ld entries)
     for (int64_t j = int64_t(blockIdx.x) * NT + threadIdx.x; j < a.ld; j += int64_t(G) * NT)
       a.wc[j] = j < a.n ? __ldg(a.xin + j) : 0.0;
     grid.sync();
-    phase_b(a, a.wc, r0, r1, a.sv, sh);
+    phase_b(plan_view(a, r0, r1), a.wc, r0, r1, a.sv, sh);
     for (int64_t i = r0 + threadIdx.x; i < r1; i += NT) a.d[i] = a.sv[i];
   }
   res.hvps = nh;
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.res = res;
 }
 
-cudaError_t launch_coop(otn_ctx* x, const CoopArgs& a) {
-  void* args[] = {const_cast<CoopArgs*>(&a)};
-  return cudaLaunchCooperativeKernel((void*)k_coop, dim3(x->coop_blocks), dim3(NT), args, 0,
-                                     x->stream);
+constexpr size_t kRingBytes = size_t(kRingDepth) * CH * NT * sizeof(double2);
+
+cudaError_t launch_coop(otn_ctx* x, const CoopArgs& a0) {
+  CoopArgs a = a0;
+  a.stages = kRingDepth;
+  void* args[] = {&a};
+  return cudaLaunchCooperativeKernel((void*)k_coop, dim3(x->coop_blocks), dim3(NT), args,
+                                     kRingBytes, x->stream);
 }
 
 int coop_occupancy(int* blocks_per_sm) {
-  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_coop, NT, 0);
+  cudaError_t e = cudaFuncSetAttribute(k_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(kRingBytes));
+  if (e != cudaSuccess) return int(e);
+  return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_coop, NT,
+                                                            kRingBytes);
 }
 
 }  // namespace otn

@@ -13,6 +13,8 @@ constexpr int kLseThreads = 256;        // 8 warps: one row per warp
 constexpr int kColTile = 64;            // columns per CTA in column reductions
 constexpr int kRedSlots = 2;            // rotating grid-reduction slots
 constexpr int kRedWidth = 4;            // doubles per CTA per slot
+constexpr int kSegCols = 64;            // plan segment (zero-skip granularity): 64 cols = 512 B
+constexpr int kSegWordCols = 64 * kSegCols;  // columns covered by one 64-bit mask word
 
 // Device-side solver record (mirrored by otn_solve_result on the host).
 struct DevResult {
@@ -62,14 +64,15 @@ cudaError_t launch_lse_cols(otn_ctx* x, const double* C, double ng, const double
                             double alpha, int mode, double* out);
 cudaError_t launch_materialize(otn_ctx* x, const double* C, double ng, const double* u,
                                const double* v, double* P, const double* icP, const double* rP,
-                               double* mu, int* flag);
+                               double* mu, int* flag, uint64_t* mask);
+cudaError_t launch_plan_mask(otn_ctx* x, const double* P, uint64_t* mask);
 cudaError_t launch_sys_prep(otn_ctx* x, const double* log_rP, const double* log_cP, double* rP,
                             double* cP, double* icP, int* flag);
 cudaError_t launch_square_matvec(otn_ctx* x, const double* P, const double* w, double* out);
 
 // Persistent cooperative solver.
 enum CoopMode { kModeNewton = 0, kModePcg = 1, kModeHvp = 2, kModePc = 3, kModeMatvec = 4,
-                kModeRmatvec = 5 };
+                kModeRmatvec = 5, kModeProbe = 6 };
 struct CoopArgs {
   const double* P;
   int64_t n, ld;
@@ -85,6 +88,10 @@ struct CoopArgs {
   int zero_init, has_x0, mode, pad;
   int64_t max_iters;
   const int* pre_flags;   // materialize / prep flags checked first (nullable)
+  const uint64_t* mask;   // plan segment occupancy (nullable = dense); mw words per row
+  int64_t mw;
+  int stages;             // shared-memory ring stages (set by launch_coop)
+  int pad2;
   // workspace
   double *r, *z, *p, *q, *M, *wc, *sv, *wpart, *red;
   DevResult* res;

@@ -159,18 +159,21 @@ __global__ void k_lse_cols_fin(LseArgs a, int slabs, const double* part) {
 __global__ void __launch_bounds__(kLseThreads) k_materialize(const double* __restrict__ C,
     int64_t n, int64_t ld, double ng, const double* __restrict__ u, const double* __restrict__ v,
     double* __restrict__ P, const double* __restrict__ icP, const double* __restrict__ rP,
-    double* __restrict__ mu, int* __restrict__ flag) {
+    double* __restrict__ mu, int* __restrict__ flag, uint64_t* __restrict__ mask) {
   const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
   const double* crow = C + row * ld;
   double* prow = P + row * ld;
   const double ui = __ldg(u + row);
+  const int64_t mw = (ld + kSegWordCols - 1) / kSegWordCols;
   double acc = 0.0, mx = OTN_NINF;
+  uint64_t bits = 0;
   for (int64_t base = 0; base < ld; base += 256) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t j = base + 64 * k + 2 * lane;
+      bool nz = false;
       if (j < ld) {
         double e0 = OTN_NINF, e1 = OTN_NINF;
         if (j < n) {
@@ -181,11 +184,18 @@ __global__ void __launch_bounds__(kLseThreads) k_materialize(const double* __res
         mx = fmax(mx, fmax(e0, e1));
         const double p0 = exp(e0), p1 = exp(e1);
         *reinterpret_cast<double2*>(prow + j) = make_double2(p0, p1);
+        nz = (p0 != 0.0) || (p1 != 0.0);
         if (icP) {
           if (j < n) acc = fma(__dmul_rn(p0, p0), __ldg(icP + j), acc);
           if (j + 1 < n) acc = fma(__dmul_rn(p1, p1), __ldg(icP + j + 1), acc);
         }
       }
+      // segment (64 columns = 512 B) occupancy bit for the HVP's zero skipping
+      if (__ballot_sync(0xffffffffu, nz)) bits |= 1ull << (((base >> 6) + k) & 63);
+    }
+    if (mask && (((base + 256) % kSegWordCols) == 0 || base + 256 >= ld)) {
+      if (lane == 0) mask[row * mw + base / kSegWordCols] = bits;
+      bits = 0;
     }
   }
   mx = warp_max(mx);
@@ -193,6 +203,30 @@ __global__ void __launch_bounds__(kLseThreads) k_materialize(const double* __res
   if (lane == 0) {
     if (mx > 700.0) atomicOr(flag, 1);          // _kernels.py:53-58
     if (icP) mu[row] = __ddiv_rn(acc, __ldg(rP + row));
+  }
+}
+
+// Segment occupancy mask of an externally supplied plan (same layout as the
+// mask written by k_materialize).
+__global__ void __launch_bounds__(kLseThreads) k_plan_mask(const double* __restrict__ P,
+    int64_t n, int64_t ld, uint64_t* __restrict__ mask) {
+  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const int64_t mw = (ld + kSegWordCols - 1) / kSegWordCols;
+  uint64_t bits = 0;
+  for (int64_t base = 0; base < ld; base += 64) {
+    const int64_t j = base + 2 * lane;
+    bool nz = false;
+    if (j < ld) {
+      const double2 p = ld_stream2(P + row * ld + j);
+      nz = (p.x != 0.0) || (p.y != 0.0);
+    }
+    if (__ballot_sync(0xffffffffu, nz)) bits |= 1ull << ((base >> 6) & 63);
+    if (((base + 64) % kSegWordCols) == 0 || base + 64 >= ld) {
+      if (lane == 0) mask[row * mw + base / kSegWordCols] = bits;
+      bits = 0;
+    }
   }
 }
 
@@ -254,9 +288,14 @@ cudaError_t launch_lse_cols(otn_ctx* x, const double* C, double ng, const double
 
 cudaError_t launch_materialize(otn_ctx* x, const double* C, double ng, const double* u,
                                const double* v, double* P, const double* icP, const double* rP,
-                               double* mu, int* flag) {
+                               double* mu, int* flag, uint64_t* mask) {
   k_materialize<<<rows_grid(x->n), kLseThreads, 0, x->stream>>>(C, x->n, x->ld, ng, u, v, P, icP,
-                                                                 rP, mu, flag);
+                                                                 rP, mu, flag, mask);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plan_mask(otn_ctx* x, const double* P, uint64_t* mask) {
+  k_plan_mask<<<rows_grid(x->n), kLseThreads, 0, x->stream>>>(P, x->n, x->ld, mask);
   return cudaGetLastError();
 }
 

@@ -250,27 +250,27 @@ class DualState:
 
     # -- plan --------------------------------------------------------------------
     def _materialize(self, reuse_buffer=False, icP=None, rP=None, mu=None, check=True):
-        """Device plan P (n x ld); optional fused Jacobi diagonal (K4 + K5)."""
+        """Device plan (P n x ld, segment mask); optional fused Jacobi diagonal (K4 + K5)."""
         opcount.add(4)
         self._touch_K()
         k = self._ctx
         if reuse_buffer:
             if self._plan_buf is None:
-                self._plan_buf = k.mat()
-            P = self._plan_buf
+                self._plan_buf = (k.mat(), k.seg_mask())
+            P, mask = self._plan_buf
         else:
-            P = k.mat()
+            P, mask = k.mat(), k.seg_mask()
         flag = ctypes.c_int(0)
         rc = k.call("otn_materialize", self._dc.ptr(), self._ng, vptr(self._u), vptr(self._v),
                     vptr(P), vptr(icP), vptr(rP), vptr(mu),
-                    ctypes.byref(flag) if check else None)
+                    ctypes.byref(flag) if check else None, vptr(mask))
         if rc == _lib.OTN_ST_PLAN_OVERFLOW:
             _lib.raise_for_status(rc, "materialize_plan")
-        return P
+        return P, mask
 
     def materialize_plan(self, reuse_buffer=False):
         """Linear-domain plan (dual.py:155-169); host array for host problems."""
-        P = self._materialize(reuse_buffer=reuse_buffer)
+        P, _ = self._materialize(reuse_buffer=reuse_buffer)
         if is_tensor(self.problem.C):
             return P[:, : self.n]
         return P[:, : self.n].cpu().numpy()

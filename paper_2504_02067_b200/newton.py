@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib, opcount
-from ._device import Context, is_tensor, require_cuda, vptr
+from ._device import TELEMETRY, Context, is_tensor, require_cuda, torch, vptr
 from .errors import ConditioningError, NonconvergenceError, StagnationError
 
 RHO_CAP = 1e-12               # newton.py:32
@@ -51,7 +51,7 @@ class DiscountedSystem:
     the Jacobi diagonal (one fused pass, K4 + K5).
     """
 
-    def __init__(self, P, rP, cP, *, _ctx=None, _mu=None, _icP=None):
+    def __init__(self, P, rP, cP, *, _ctx=None, _mu=None, _icP=None, _mask=None):
         if _ctx is None:
             rP_h = rP.detach().cpu().numpy() if is_tensor(rP) else np.asarray(rP, dtype=np.float64)
             cP_h = cP.detach().cpu().numpy() if is_tensor(cP) else np.asarray(cP, dtype=np.float64)
@@ -71,11 +71,14 @@ class DiscountedSystem:
             self._cP = ctx.vec(cP_h)
             self._icP = ctx.vec(1.0 / cP_h)
             self._mu_dev = None
+            self._mask = ctx.seg_mask()
+            ctx.call("otn_plan_mask", vptr(Pd), vptr(self._mask))
         else:
             self._ctx = _ctx
             self._P, self._rP, self._cP = P, rP, cP
             self._icP = _icP
             self._mu_dev = _mu
+            self._mask = _mask
         self.n = self._ctx.n
         self._mu_counted = False
 
@@ -91,14 +94,14 @@ class DiscountedSystem:
         rP, cP, icP, mu = bufs
         lr, lc = state._lr_dev(), state._lc_dev()
         ctx.call("otn_system_prep", vptr(lr), vptr(lc), vptr(rP), vptr(cP), vptr(icP), None)
-        P = state._materialize(reuse_buffer=True, icP=icP, rP=rP, mu=mu, check=False)
+        P, mask = state._materialize(reuse_buffer=True, icP=icP, rP=rP, mu=mu, check=False)
         flags = (ctypes.c_int * 4)()
         ctx.call("otn_read_flags", flags)
         if flags[0]:
             _lib.raise_for_status(_lib.OTN_ST_PLAN_OVERFLOW, "materialize_plan")
         if flags[1]:
             _lib.raise_for_status(_lib.OTN_ST_NONPOSITIVE_SUMS, "DiscountedSystem")
-        return cls(P, rP, cP, _ctx=ctx, _mu=mu, _icP=icP)
+        return cls(P, rP, cP, _ctx=ctx, _mu=mu, _icP=icP, _mask=mask)
 
     # -- host views for API parity ---------------------------------------------
     @property
@@ -125,7 +128,8 @@ class DiscountedSystem:
         """P_c d = (P^T d)/cP (newton.py:96-98)."""
         opcount.add(1)
         out = self._ctx.vec()
-        self._ctx.call("otn_apply_pc", vptr(self._P), vptr(self._cP), vptr(self._in(d)), vptr(out))
+        self._ctx.call("otn_apply_pc", vptr(self._P), vptr(self._mask), vptr(self._cP),
+                       vptr(self._in(d)), vptr(out))
         return _as_host(d, out, self._ctx)
 
     def apply_prc(self, d):
@@ -133,9 +137,10 @@ class DiscountedSystem:
         opcount.add(2)
         k = self._ctx
         w = k.vec()
-        k.call("otn_apply_pc", vptr(self._P), vptr(self._cP), vptr(self._in(d)), vptr(w))
+        k.call("otn_apply_pc", vptr(self._P), vptr(self._mask), vptr(self._cP), vptr(self._in(d)),
+               vptr(w))
         s = k.vec()
-        k.call("otn_matvec", vptr(self._P), vptr(w), vptr(s))
+        k.call("otn_matvec", vptr(self._P), vptr(self._mask), vptr(w), vptr(s))
         out = s / self._rP.clamp_min(np.finfo(np.float64).tiny)
         return _as_host(d, out, k)
 
@@ -144,8 +149,8 @@ class DiscountedSystem:
         if rho != 0.0:
             opcount.add(2)
         out = self._ctx.vec()
-        self._ctx.call("otn_apply_F", vptr(self._P), vptr(self._rP), vptr(self._cP), float(rho),
-                       vptr(self._in(d)), vptr(out))
+        self._ctx.call("otn_apply_F", vptr(self._P), vptr(self._mask), vptr(self._rP),
+                       vptr(self._cP), float(rho), vptr(self._in(d)), vptr(out))
         return _as_host(d, out, self._ctx)
 
     def _tally_mu(self):
@@ -210,7 +215,8 @@ def pcg_solve(sys, rho, b, tol_l1, d0=None, max_iters=None):
     bd = sys._in(b)
     x = k.vec(d0) if d0 is not None else k.vec()
     res = _lib.SolveResult()
-    rc = k.call("otn_pcg", vptr(sys._P), vptr(sys._rP), vptr(sys._cP), vptr(mu), float(rho),
+    rc = k.call("otn_pcg", vptr(sys._P), vptr(sys._mask), vptr(sys._rP), vptr(sys._cP), vptr(mu),
+                float(rho),
                 vptr(bd), float(tol_l1), vptr(x), int(d0 is not None), int(max_iters),
                 ctypes.byref(res))
     opcount.add(2 * int(res.hvps))
@@ -226,9 +232,18 @@ def _newton_device(grad_u, sys, eta, rho0, zero_init, max_cg_iters, d_u, d_v):
     if max_cg_iters is None:
         max_cg_iters = 10 * sys.n
     res = _lib.SolveResult()
-    k.call("otn_newton", vptr(sys._P), vptr(sys._rP), vptr(sys._cP), vptr(sys._mu()),
+    timed = TELEMETRY.time_coop
+    if timed:
+        t = torch()
+        ev0, ev1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+        ev0.record()
+    k.call("otn_newton", vptr(sys._P), vptr(sys._mask), vptr(sys._rP), vptr(sys._cP),
+           vptr(sys._mu()),
            vptr(grad_u), float(eta), float(rho0), int(bool(zero_init)), int(max_cg_iters),
            vptr(d_u), vptr(d_v), ctypes.byref(res))
+    if timed:
+        ev1.record()
+        TELEMETRY.coop.append((ev0, ev1, int(res.hvps), int(d_v is not None), k.n))
     if res.pcg_calls > 0:
         sys._tally_mu()
     opcount.add(2 * int(res.hvps))

@@ -143,6 +143,25 @@ def run_case(name, spec, gi, gf, verify_oracle):
     )
     arrays = dict(u=st.u.copy(), v=st.v.copy(),
                   P_rowsum=sol.P.sum(axis=1), P_colsum=sol.P.sum(axis=0))
+    # The reference's own reduction-order noise floor: rerun with
+    # OTN_DETERMINISTIC=1 (fixed-order matvecs instead of BLAS, opcount.py:89-91)
+    # and record how far the trajectory and potentials move.
+    os.environ["OTN_DETERMINISTIC"] = "1"
+    try:
+        ref_opcount.reset()
+        det = ref.mdot(ref.Problem(C=prob.C, r=prob.r, c=prob.c), gi, gf)
+    finally:
+        del os.environ["OTN_DETERMINISTIC"]
+    du_det = float(np.abs(det.final_state.u - st.u).max() / np.abs(st.u).max())
+    dv_det = float(np.abs(det.final_state.v - st.v).max() / np.abs(st.v).max())
+    meta["self_spread"] = dict(
+        stages=len(det.iterations),
+        newton=[i.stats.newton_steps for i in det.iterations],
+        cg=[i.stats.cg_iters for i in det.iterations],
+        cg_total=sum(i.stats.cg_iters for i in det.iterations),
+        du=du_det, dv=dv_det, primal=det.primal_cost)
+    print(f"  self-spread (BLAS vs deterministic): stages {len(det.iterations)} "
+          f"cg {meta['self_spread']['cg_total']} vs {meta['totals']['cg']}, du={du_det:.2e}")
     if prob.n <= 64:
         arrays["P"] = sol.P.copy()
     if verify_oracle:
