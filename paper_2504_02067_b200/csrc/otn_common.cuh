@@ -35,6 +35,41 @@ __device__ __forceinline__ double2 ld_stream2(const double* p) {
   return r;
 }
 
+// Branch-free float64 exp (max error ~1 ulp), used for every plan entry.
+// CUDA's exp(double) takes a divergent slow path for |x| > 708, which is where
+// most plan exponents live at weak regularization (they underflow to 0).
+// Cody-Waite reduction x = k ln2 + r, |r| <= ln2/2, degree-13 Taylor
+// polynomial in Horner form, and 2^k applied as two exact power-of-two factors
+// so subnormal results are rounded once and underflow / overflow come out as
+// 0 / inf.  x < -746 -> 0, x > 710 -> inf, NaN -> NaN.
+__device__ __forceinline__ double pow2i(int e) {        // 2^e, -1022 <= e <= 1023
+  return __hiloint2double((e + 1023) << 20, 0);
+}
+// Coefficients live in the constant bank so DFMA reads them directly (a
+// double immediate would cost two uniform moves per use inside hot loops).
+__constant__ double kExpPoly[14] = {
+    1.6059043836821614599e-10, 2.0876756987868098979e-09, 2.5052108385441718775e-08,
+    2.7557319223985890653e-07, 2.7557319223985890653e-06, 2.4801587301587301587e-05,
+    1.9841269841269841270e-04, 1.3888888888888888889e-03, 8.3333333333333333333e-03,
+    4.1666666666666666667e-02, 1.6666666666666666667e-01, 0.5, 1.0, 1.0};
+__constant__ double kExpRed[3] = {1.4426950408889634, 6.93147180369123816490e-01,
+                                  1.90821492927058770002e-10};
+
+__device__ __forceinline__ double exp_fast(double x) {
+  x = x < -746.0 ? -746.0 : (x > 710.0 ? 710.0 : x);
+  // k = round(x / ln2) via the 1.5*2^52 shifter: no FRND / F2I conversions
+  const double t = fma(x, kExpRed[0], 6755399441055744.0);
+  const int k = __double2loint(t);
+  const double kd = t - 6755399441055744.0;
+  double r = fma(-kd, kExpRed[1], x);                     // ln2_hi (exact product)
+  r = fma(-kd, kExpRed[2], r);                            // ln2_lo
+  double p = kExpPoly[0];                                 // 1/13! ... 1/0! (Horner)
+#pragma unroll
+  for (int i = 1; i < 14; ++i) p = fma(p, r, kExpPoly[i]);
+  const int k1 = k >> 1;
+  return (p * pow2i(k1)) * pow2i(k - k1);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -51,10 +86,10 @@ __device__ __forceinline__ double warp_max(double v) {
 // represents m + log(s) and m = -inf encodes an empty / all -inf set.
 __device__ __forceinline__ void lse_merge(double& m, double& s, double m2, double s2) {
   if (m2 > m) {
-    s = __dadd_rn(__dmul_rn(s, exp(m - m2)), s2);
+    s = __dadd_rn(__dmul_rn(s, exp_fast(m - m2)), s2);
     m = m2;
   } else if (m2 != OTN_NINF) {
-    s = __dadd_rn(s, __dmul_rn(s2, exp(m2 - m)));
+    s = __dadd_rn(s, __dmul_rn(s2, exp_fast(m2 - m)));
   }
 }
 

@@ -66,12 +66,12 @@ __global__ void __launch_bounds__(kLseThreads) k_lse_rows(LseArgs a) {
 #pragma unroll
     for (int k = 1; k < 8; ++k) cm = fmax(cm, b[k]);
     if (cm > m) {
-      s = s * exp(m - cm);
+      s = s * exp_fast(m - cm);
       m = cm;
     }
     if (m != OTN_NINF) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) s += exp(b[k] - m);
+      for (int k = 0; k < 8; ++k) s += exp_fast(b[k] - m);
     }
   }
   warp_lse(m, s);
@@ -111,15 +111,15 @@ __global__ void __launch_bounds__(kLseThreads) k_lse_cols_part(LseArgs a, int64_
     }
     double cm0 = fmax(fmax(b0[0], b0[1]), fmax(b0[2], b0[3]));
     double cm1 = fmax(fmax(b1[0], b1[1]), fmax(b1[2], b1[3]));
-    if (cm0 > m0) { s0 = s0 * exp(m0 - cm0); m0 = cm0; }
-    if (cm1 > m1) { s1 = s1 * exp(m1 - cm1); m1 = cm1; }
+    if (cm0 > m0) { s0 = s0 * exp_fast(m0 - cm0); m0 = cm0; }
+    if (cm1 > m1) { s1 = s1 * exp_fast(m1 - cm1); m1 = cm1; }
     if (m0 != OTN_NINF) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) s0 += exp(b0[k] - m0);
+      for (int k = 0; k < 4; ++k) s0 += exp_fast(b0[k] - m0);
     }
     if (m1 != OTN_NINF) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) s1 += exp(b1[k] - m1);
+      for (int k = 0; k < 4; ++k) s1 += exp_fast(b1[k] - m1);
     }
   }
   sm_m[warp][2 * lane] = m0;
@@ -153,7 +153,7 @@ __global__ void k_lse_cols_fin(LseArgs a, int slabs, const double* part) {
 }
 
 // ---------------------------------------------------------------------------
-// Plan: P_ij = exp((ng*C_ij + v_j) + u_i), one warp per row, 16-byte stores,
+// Plan: P_ij = exp_fast((ng*C_ij + v_j) + u_i), one warp per row, 16-byte stores,
 // zeros in the padding columns.  Fused K5: mu_i = (sum_j P_ij^2 icP_j)/rP_i.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kLseThreads) k_materialize(const double* __restrict__ C,
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kLseThreads) k_materialize(const double* __res
           if (j + 1 < n) e1 = __dadd_rn(__dadd_rn(__dmul_rn(ng, c.y), __ldg(v + j + 1)), ui);
         }
         mx = fmax(mx, fmax(e0, e1));
-        const double p0 = exp(e0), p1 = exp(e1);
+        const double p0 = exp_fast(e0), p1 = exp_fast(e1);
         *reinterpret_cast<double2*>(prow + j) = make_double2(p0, p1);
         nz = (p0 != 0.0) || (p1 != 0.0);
         if (icP) {
@@ -234,7 +234,7 @@ __global__ void k_sys_prep(int64_t n, const double* __restrict__ lr, const doubl
                            double* rP, double* cP, double* icP, int* flag) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double rp = exp(lr[i]), cp = exp(lc[i]);
+  const double rp = exp_fast(lr[i]), cp = exp_fast(lc[i]);
   rP[i] = rp;
   cP[i] = cp;
   icP[i] = __ddiv_rn(1.0, cp);                  // newton.py:111: 1.0 / self.cP

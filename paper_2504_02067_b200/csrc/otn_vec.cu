@@ -20,8 +20,8 @@ __global__ void k_vec(int op, int64_t n, double s, const double* a, const double
         o = __dadd_rn(__dadd_rn(a[i], __dmul_rn(s, b[i])), __dsub_rn(c[i], d[i]));
         break;
       case OTN_VEC_EXTRAP: o = __dadd_rn(a[i], __dmul_rn(s, __dsub_rn(a[i], b[i]))); break;
-      case OTN_VEC_EXP: o = exp(a[i]); break;
-      case OTN_VEC_GRAD: o = __dsub_rn(exp(a[i]), b[i]); break;
+      case OTN_VEC_EXP: o = exp_fast(a[i]); break;
+      case OTN_VEC_GRAD: o = __dsub_rn(exp_fast(a[i]), b[i]); break;
       default: o = 0.0;
     }
     out[i] = o;
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(1024) k_reduce(int op, int64_t n, const double
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     switch (op) {
       case OTN_RED_ROW_STATS: {
-        const double x = exp(a[i]), y = b[i];
+        const double x = exp_fast(a[i]), y = b[i];
         s0 += fabs(__dsub_rn(x, y));
         s1 += __ddiv_rn(__dmul_rn(y, y), x);
         if (x <= 0.0) f |= 1;
@@ -48,10 +48,10 @@ __global__ void __launch_bounds__(1024) k_reduce(int op, int64_t n, const double
         break;
       }
       case OTN_RED_GRAD_L1:
-        s0 += fabs(__dsub_rn(exp(a[i]), b[i]));
-        s1 += fabs(__dsub_rn(exp(c[i]), d[i]));
+        s0 += fabs(__dsub_rn(exp_fast(a[i]), b[i]));
+        s1 += fabs(__dsub_rn(exp_fast(c[i]), d[i]));
         break;
-      case OTN_RED_SUM_EXP: s0 += exp(a[i]); break;
+      case OTN_RED_SUM_EXP: s0 += exp_fast(a[i]); break;
       case OTN_RED_DOT: s0 = fma(a[i], b[i], s0); break;
       case OTN_RED_L1: s0 += fabs(a[i]); break;
       default: break;

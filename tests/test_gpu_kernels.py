@@ -182,3 +182,33 @@ def test_rho_anneals_on_quarter_grid():
     assert k == pytest.approx(round(k), abs=1e-9)
     resid = sysd.apply_F(1.0, res.d_u) + grad
     assert np.abs(resid).sum() <= 0.01 * np.abs(grad).sum() + 1e-15
+
+
+def test_exp_fast_accuracy():
+    """The kernels' branch-free exp vs numpy: <= 1 ulp over the whole range,
+    exact 0 / inf / NaN at the ends (used for every plan entry)."""
+    import torch
+    from paper_2504_02067_b200 import _lib
+    from paper_2504_02067_b200._device import Context, require_cuda, vptr
+    rng = np.random.default_rng(0)
+    x = np.concatenate([rng.uniform(-750, 712, 200000), rng.uniform(-1, 1, 50000),
+                        rng.uniform(-746, -700, 50000),
+                        [0.0, -0.0, 1.0, -1.0, -745.1, -745.2, -744.4, 709.78, 709.79, 710.0,
+                         -np.inf, np.inf, np.nan, 1e-300, -1e-300]])
+    n = 8192
+    x = np.concatenate([x, np.zeros((-x.size) % n)])
+    ctx = Context.get(n, require_cuda())
+    got = np.empty_like(x)
+    for k in range(0, x.size, n):
+        a = ctx.vec(x[k:k + n])
+        out = ctx.vec()
+        ctx.call("otn_vec", _lib.VEC_EXP, 0.0, vptr(a), None, None, None, vptr(out))
+        got[k:k + n] = ctx.download(out)
+    want = np.exp(x)
+    both_nan = np.isnan(got) & np.isnan(want)
+    assert np.all(both_nan == np.isnan(want))
+    ok = ~np.isnan(want)
+    g, w = got[ok], want[ok]
+    # ulp distance on the IEEE bit patterns (monotone for non-negative doubles)
+    ulps = np.abs(g.view(np.int64) - w.view(np.int64))
+    assert ulps.max() <= 1, (ulps.max(), x[ok][np.argmax(ulps)])
