@@ -54,7 +54,19 @@ enum otn_vec_op {
   OTN_VEC_STEP_V = 2,   /* out = (a + s*b) + (c - d) projector.py:235                       */
   OTN_VEC_EXTRAP = 3,   /* out = a + s*(a - b)      driver.py:170-175                       */
   OTN_VEC_EXP = 4,      /* out = exp(a)             dual.py:134-138                         */
-  OTN_VEC_GRAD = 5      /* out = exp(a) - b         projector.py:176                        */
+  OTN_VEC_GRAD = 5,     /* out = exp(a) - b         projector.py:176                        */
+  OTN_VEC_MUL_SUB = 6,  /* out = a*b - s*c          newton.py:102-105 (rP*d - rho*P(..))    */
+  OTN_VEC_DIV = 7,      /* out = a / b              newton.py:98,112,158                    */
+  OTN_VEC_SUB = 8,      /* out = a - b              newton.py:146,164                       */
+  OTN_VEC_ADD = 9,      /* out = a + b              newton.py:199                           */
+  OTN_VEC_PRECOND = 10, /* out = a * (1 - s*b)      newton.py:137                           */
+  OTN_VEC_NEG_DIV = 11, /* out = (-a) / b           newton.py:192, projector.py:201         */
+  OTN_VEC_RESCALE = 12, /* out = a * exp(b - c)     (sharded column-LSE combine)            */
+  OTN_VEC_LSE_FIN = 13, /* out = a + (b finite ? b + log(c) : -inf)   _kernels.py:36-42     */
+  OTN_VEC_LSE_FIN_SUB = 14, /* out = a - (b finite ? b + log(c) : -inf)  dual.py:182        */
+  OTN_VEC_ROUND_SCALE = 15, /* out = b > 0 ? min(1, a / b) : 1          driver.py:193,198     */
+  OTN_VEC_SUB_MUL = 16, /* out = a - b*c              driver.py:201-202                     */
+  OTN_VEC_MUL = 17      /* out = a * b                newton.py:102                         */
 };
 
 /* Reductions for otn_reduce; results go to host_out[0..1]. */
@@ -64,7 +76,22 @@ enum otn_reduce_op {
   OTN_RED_GRAD_L1 = 1,   /* [sum|exp(a)-b|, sum|exp(c)-d|]   dual.py:142-148              */
   OTN_RED_SUM_EXP = 2,   /* [sum exp(a)]                      projector.py:122-126         */
   OTN_RED_DOT = 3,       /* [sum a*b]                         dual.py:150-153              */
-  OTN_RED_L1 = 4         /* [sum |a|]                                                      */
+  OTN_RED_L1 = 4,        /* [sum |a|]                                                      */
+  OTN_RED_L1_ADD = 5,    /* [sum |a + b|]                     newton.py:199-200            */
+  OTN_RED_NONPOS = 6,    /* [count(a <= 0)]                   newton.py:138                */
+  OTN_RED_MAX = 7,       /* [max a]                                                        */
+  OTN_RED_L1_DOT = 8     /* [sum |a|, sum a*b]                newton.py:162-165            */
+};
+
+/* Point-cloud pass operations for otn_pc_pass. */
+enum otn_pc_op {
+  OTN_PC_LSE = 0,   /* out_i = outer_i +/- LSE_j(e_ij)                                     */
+  OTN_PC_DOT = 1,   /* out_i = sum_j exp(e_ij) vec_j                                       */
+  OTN_PC_DIAG = 2,  /* out_i = sum_j exp(e_ij)^2 vec_j; out2_i = max_j e_ij                */
+  OTN_PC_MAXD = 3,  /* out_i = max_j D_ij (raw squared distance; pass cmax = 0)             */
+  OTN_PC_LSE_PART = 4, /* out_i = max_j e_ij, out2_i = sum_j exp(e_ij - out_i) (shard partial) */
+  OTN_PC_DOTC = 5,  /* out_i = sum_j exp(e_ij) C_ij vec_j   (primal cost <P, C>)            */
+  OTN_PC_CDOT = 6   /* out_i = sum_j C_ij vec_j             (rank-one term of <P, C>)       */
 };
 
 typedef struct otn_ctx otn_ctx;
@@ -175,6 +202,32 @@ int otn_newton(otn_ctx* ctx, const double* P, const uint64_t* seg_mask, const do
  * 3 row pass, 4 P^T x with its reductions, 5 full HVP).  Tooling only.     */
 int otn_probe(otn_ctx* ctx, const double* P, const uint64_t* seg_mask, const double* cP,
               const double* rP, const double* x, double* out, int what, int64_t reps);
+
+/* ---- on-the-fly point-cloud cost (D4/D5; no n x n array anywhere) ----------
+ * One pass over all (row point a_i, column point b_j) pairs of the two SoA
+ * point sets A (na points, lda stride between coordinates) and B:
+ *   C_ij = (sum_k (a_ik - b_jk)^2) / cmax  (left-to-right sum, IEEE division:
+ *          bit-identical to PointCloudProblem.materialize_cost),
+ *   e_ij = order 0: (neg_gamma*C_ij + colpot_j) + rowpot_i
+ *          order 1: (neg_gamma*C_ij + rowpot_i) + colpot_j
+ *   with colpot_j += alpha*colpot_d_j when colpot_d != NULL and absent
+ *   potentials treated as "not added".
+ * Row passes of the reference's operators use A = X, B = Y; column passes
+ * (P^T x, column LSE: log_plan_row_sums(K^T, ...), dual.py:97-175) swap the
+ * point sets and use order 1 so the exponent keeps the reference's rounding
+ * ((K + v) + u, _kernels.py:52-53).  For a row-sharded solve A holds this
+ * rank's rows; column passes then produce per-rank partials the caller
+ * combines with an allreduce.                                                */
+int otn_pc_pass(otn_ctx* ctx, int op, const double* A, int64_t na, int64_t lda, const double* B,
+                int64_t nb, int64_t ldb, int d, double cmax, double neg_gamma, int order,
+                const double* colpot, const double* colpot_d, double alpha, const double* rowpot,
+                const double* vec, const double* outer, const double* outer_d, int mode,
+                double* out, double* out2);
+/* Element-wise op / reduction on explicit lengths (sharded vectors). */
+int otn_vec_n(otn_ctx* ctx, int64_t n, int op, double s, const double* a, const double* b,
+              const double* c, const double* d, double* out);
+int otn_reduce_n(otn_ctx* ctx, int64_t n, int op, const double* a, const double* b,
+                 const double* c, const double* d, double* host_out, int* host_flags);
 
 /* ---- projector / driver vector work ------------------------------------- */
 int otn_vec(otn_ctx* ctx, int op, double s, const double* a, const double* b, const double* c,

@@ -33,8 +33,12 @@ OTN_ST_NONCONVERGENCE = 14
 OTN_ST_STAGNATION = 15
 OTN_ST_DOMAIN = 16
 
-VEC_ADD_SUB, VEC_AXPY, VEC_STEP_V, VEC_EXTRAP, VEC_EXP, VEC_GRAD = range(6)
-RED_ROW_STATS, RED_GRAD_L1, RED_SUM_EXP, RED_DOT, RED_L1 = range(5)
+(VEC_ADD_SUB, VEC_AXPY, VEC_STEP_V, VEC_EXTRAP, VEC_EXP, VEC_GRAD, VEC_MUL_SUB, VEC_DIV,
+ VEC_SUB, VEC_ADD, VEC_PRECOND, VEC_NEG_DIV, VEC_RESCALE, VEC_LSE_FIN, VEC_LSE_FIN_SUB,
+ VEC_ROUND_SCALE, VEC_SUB_MUL, VEC_MUL) = range(18)
+(RED_ROW_STATS, RED_GRAD_L1, RED_SUM_EXP, RED_DOT, RED_L1, RED_L1_ADD, RED_NONPOS,
+ RED_MAX, RED_L1_DOT) = range(9)
+PC_LSE, PC_DOT, PC_DIAG, PC_MAXD, PC_LSE_PART, PC_DOTC, PC_CDOT = range(7)
 
 
 class SolveResult(ctypes.Structure):
@@ -83,6 +87,10 @@ SIGNATURES = {
     "otn_newton": [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I, _I64, _P, _P,
                    ctypes.POINTER(SolveResult)],
     "otn_probe": [_P, _P, _P, _P, _P, _P, _P, _I, _I64],
+    "otn_pc_pass": [_P, _I, _P, _I64, _I64, _P, _I64, _I64, _I, _D, _D, _I, _P, _P, _D, _P, _P,
+                    _P, _P, _I, _P, _P],
+    "otn_vec_n": [_P, _I64, _I, _D, _P, _P, _P, _P, _P],
+    "otn_reduce_n": [_P, _I64, _I, _P, _P, _P, _P, _DP, _IP],
     "otn_vec": [_P, _I, _D, _P, _P, _P, _P, _P],
     "otn_reduce": [_P, _I, _P, _P, _P, _P, _DP, _IP],
     "otn_round_plan": [_P, _P, _P, _P, _P, _DP, _IP],

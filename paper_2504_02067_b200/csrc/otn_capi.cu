@@ -396,11 +396,56 @@ int otn_probe(otn_ctx* x, const double* P, const uint64_t* m, const double* cP, 
   return OTN_OK;
 }
 
+// ---- point clouds ------------------------------------------------------------
+int otn_pc_pass(otn_ctx* x, int op, const double* A, int64_t na, int64_t lda, const double* B,
+                int64_t nb, int64_t ldb, int d, double cmax, double ng, int order,
+                const double* colpot, const double* colpot_d, double alpha, const double* rowpot,
+                const double* vec, const double* outer, const double* outer_d, int mode,
+                double* out, double* out2) {
+  OTN_REQUIRE(x && A && B && out, "otn_pc_pass: NULL argument");
+  OTN_REQUIRE(d >= 1 && d <= 4, "otn_pc_pass: point dimension must be 1..4");
+  OTN_REQUIRE(na >= 1 && nb >= 1 && lda >= na && ldb >= nb, "otn_pc_pass: bad sizes");
+  OTN_REQUIRE(op >= OTN_PC_LSE && op <= OTN_PC_CDOT, "otn_pc_pass: bad op");
+  OTN_REQUIRE((op != OTN_PC_DOT && op != OTN_PC_DIAG && op != OTN_PC_DOTC && op != OTN_PC_CDOT) ||
+                  vec != nullptr, "otn_pc_pass: DOT/DIAG/DOTC/CDOT need vec");
+  OTN_REQUIRE(op != OTN_PC_LSE_PART || out2 != nullptr, "otn_pc_pass: LSE_PART needs out2");
+  otn::PairArgs p{A, na, lda, B, nb, ldb, d, op, order, mode, cmax, ng, colpot, colpot_d, rowpot,
+                  alpha, vec, outer, outer_d, out, out2};
+  OTN_CUDA(otn::launch_pair(x, p), "otn_pc_pass");
+  return OTN_OK;
+}
+
+int otn_vec_n(otn_ctx* x, int64_t n, int op, double s, const double* a, const double* b,
+              const double* c, const double* d, double* out) {
+  OTN_REQUIRE(x && a && out && n >= 0, "otn_vec_n: bad argument");
+  OTN_REQUIRE(op >= OTN_VEC_ADD_SUB && op <= OTN_VEC_MUL, "otn_vec_n: bad op");
+  if (n == 0) return OTN_OK;
+  OTN_CUDA(otn::launch_vec(x, op, n, s, a, b, c, d, out), "otn_vec_n");
+  return OTN_OK;
+}
+
+int otn_reduce_n(otn_ctx* x, int64_t n, int op, const double* a, const double* b, const double* c,
+                 const double* d, double* host_out, int* host_flags) {
+  OTN_REQUIRE(x && a && host_out && n >= 0, "otn_reduce_n: bad argument");
+  OTN_REQUIRE(op >= OTN_RED_ROW_STATS && op <= OTN_RED_L1_DOT, "otn_reduce_n: bad op");
+  OTN_CUDA(cudaMemsetAsync(x->flags + 2, 0, sizeof(int), x->stream), "otn_reduce_n: flag");
+  OTN_CUDA(otn::launch_reduce(x, op, n, a, b, c, d, x->scal + 8, x->flags + 2), "otn_reduce_n");
+  OTN_CUDA(cudaMemcpyAsync(x->h_scal + 8, x->scal + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                           x->stream), "otn_reduce_n: copy");
+  OTN_CUDA(cudaMemcpyAsync(x->h_flags + 2, x->flags + 2, sizeof(int), cudaMemcpyDeviceToHost,
+                           x->stream), "otn_reduce_n: copy");
+  OTN_CUDA(cudaStreamSynchronize(x->stream), "otn_reduce_n: sync");
+  host_out[0] = x->h_scal[8];
+  host_out[1] = x->h_scal[9];
+  if (host_flags) *host_flags = x->h_flags[2];
+  return OTN_OK;
+}
+
 // ---- vector work -----------------------------------------------------------
 int otn_vec(otn_ctx* x, int op, double s, const double* a, const double* b, const double* c,
             const double* d, double* out) {
   OTN_REQUIRE(x && a && out, "otn_vec: NULL argument");
-  OTN_REQUIRE(op >= OTN_VEC_ADD_SUB && op <= OTN_VEC_GRAD, "otn_vec: bad op");
+  OTN_REQUIRE(op >= OTN_VEC_ADD_SUB && op <= OTN_VEC_MUL, "otn_vec: bad op");
   OTN_CUDA(otn::launch_vec(x, op, x->n, s, a, b, c, d, out), "otn_vec");
   return OTN_OK;
 }
@@ -408,7 +453,7 @@ int otn_vec(otn_ctx* x, int op, double s, const double* a, const double* b, cons
 int otn_reduce(otn_ctx* x, int op, const double* a, const double* b, const double* c,
                const double* d, double* host_out, int* host_flags) {
   OTN_REQUIRE(x && a && host_out, "otn_reduce: NULL argument");
-  OTN_REQUIRE(op >= OTN_RED_ROW_STATS && op <= OTN_RED_L1, "otn_reduce: bad op");
+  OTN_REQUIRE(op >= OTN_RED_ROW_STATS && op <= OTN_RED_L1_DOT, "otn_reduce: bad op");
   OTN_CUDA(cudaMemsetAsync(x->flags + 2, 0, sizeof(int), x->stream), "otn_reduce: flag");
   OTN_CUDA(otn::launch_reduce(x, op, x->n, a, b, c, d, x->scal + 8, x->flags + 2), "otn_reduce");
   OTN_CUDA(cudaMemcpyAsync(x->h_scal + 8, x->scal + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost,

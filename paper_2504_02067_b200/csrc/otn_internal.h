@@ -105,4 +105,24 @@ cudaError_t launch_reduce(otn_ctx* x, int op, int64_t n, const double* a, const 
                           const double* c, const double* d, double* dst, int* flag);
 cudaError_t launch_round(otn_ctx* x, double* P, const double* C, const double* r, const double* c,
                          double* scratch_scalars, int* flag);
+
+// On-the-fly point-cloud passes (otn_pc.cu).
+struct PairArgs {
+  const double* A;       // row points, SoA: A[k * lda + i]
+  int64_t na, lda;
+  const double* B;       // column points, SoA: B[k * ldb + j]
+  int64_t nb, ldb;
+  int d, op, order, mode;
+  double cmax, ng;
+  const double* colpot;    // added first (nullable)
+  const double* colpot_d;  // colpot_eff = colpot + alpha * colpot_d (nullable)
+  const double* rowpot;    // added second (nullable)
+  double alpha;
+  const double* vec;       // per-column vector (DOT / DIAG)
+  const double* outer;     // LSE: out = outer +/- lse (nullable -> 0)
+  const double* outer_d;
+  double* out;             // per-row result
+  double* out2;            // per-row aux (DIAG: max exponent; MAXD unused)
+};
+cudaError_t launch_pair(otn_ctx* x, const PairArgs& p);
 }  // namespace otn

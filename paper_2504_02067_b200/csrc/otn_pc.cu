@@ -1,0 +1,198 @@
+// On-the-fly point-cloud cost (D4/D5): every O(n^2) pass
+// recomputes C_ij = (sum_k (x_ik - y_jk)^2) / C_max and the plan entry from the
+// point coordinates instead of streaming a stored matrix.  The coordinate sum
+// runs left to right with explicit roundings and the division is IEEE, so C_ij
+// is bit-identical to the host-materialized cost (PointCloudProblem.
+// materialize_cost) and every exponent is formed with the stored path's
+// operand order: results match the stored-C kernels up to summation order.
+//
+// One register-blocked "pair" kernel serves every pass.  A CTA owns RW*8 row
+// points (RW per warp, in registers) and streams the column points in
+// shared-memory tiles of 256; lane l takes columns l, l+32, ... of a tile, so
+// each staged column is reused by all the CTA's rows.  Column passes (P^T x,
+// column LSE) are the same kernel with the two point sets swapped
+// (dist(x, y) == dist(y, x) exactly) and a flag that keeps the exponent's
+// operand order ((ng*C + v_j) + u_i).  The FP64 pipe bounds it: ~40 FP64
+// instructions per entry (distance, IEEE division, exp).
+#include "otn_common.cuh"
+#include "otn_internal.h"
+
+namespace otn {
+
+constexpr int kPcThreads = 256;     // 8 warps
+constexpr int kPcTile = 256;        // column points per shared-memory tile
+constexpr int kPcMaxDim = 4;
+
+
+
+// e_ij: order 0 -> (ng*C + colpot_j) + rowpot_i ; order 1 -> (ng*C + rowpot_i) + colpot_j
+__device__ __forceinline__ double pc_cost(const double* a, const double* b, int d, double cmax) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < kPcMaxDim; ++k) {
+    if (k < d) {
+      const double dk = __dsub_rn(a[k], b[k]);
+      s = k == 0 ? __dmul_rn(dk, dk) : __dadd_rn(s, __dmul_rn(dk, dk));
+    }
+  }
+  return cmax > 0.0 ? __ddiv_rn(s, cmax) : s;
+}
+
+template <int RW, int OP>
+__global__ void __launch_bounds__(kPcThreads, 2) k_pair(PairArgs p) {
+  __shared__ double sb[kPcMaxDim][kPcTile];
+  __shared__ double scp[kPcTile];
+  __shared__ double svec[kPcTile];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i0 = (int64_t(blockIdx.x) * 8 + warp) * RW;
+  double a[RW][kPcMaxDim], rp[RW];
+  double m[RW], s[RW];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const int64_t i = i0 + r;
+#pragma unroll
+    for (int k = 0; k < kPcMaxDim; ++k)
+      a[r][k] = (i < p.na && k < p.d) ? __ldg(p.A + k * p.lda + i) : 0.0;
+    rp[r] = (p.rowpot && i < p.na) ? __ldg(p.rowpot + i) : 0.0;
+    m[r] = (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART || OP == OTN_PC_MAXD || OP == OTN_PC_DIAG)
+               ? OTN_NINF : 0.0;
+    s[r] = 0.0;
+  }
+  for (int64_t j0 = 0; j0 < p.nb; j0 += kPcTile) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < kPcTile; t += kPcThreads) {
+      const int64_t j = j0 + t;
+      const bool ok = j < p.nb;
+#pragma unroll
+      for (int k = 0; k < kPcMaxDim; ++k)
+        sb[k][t] = (ok && k < p.d) ? __ldg(p.B + k * p.ldb + j) : 0.0;
+      double cp = 0.0;
+      if (ok && p.colpot) {
+        cp = __ldg(p.colpot + j);
+        if (p.colpot_d) cp = __dadd_rn(cp, __dmul_rn(p.alpha, __ldg(p.colpot_d + j)));
+      }
+      scp[t] = cp;
+      svec[t] = (ok && p.vec) ? __ldg(p.vec + j) : 0.0;
+    }
+    __syncthreads();
+    const int jn = int(p.nb - j0 < kPcTile ? p.nb - j0 : int64_t(kPcTile));
+    if (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART) {
+      // 8 columns per lane per tile: chunk max, one rescale, then exps
+#pragma unroll
+      for (int r = 0; r < RW; ++r) {
+        double e[8];
+        double cm = OTN_NINF;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int t = lane + 32 * q;
+          if (t < jn) {
+            double bb[kPcMaxDim];
+#pragma unroll
+            for (int k = 0; k < kPcMaxDim; ++k) bb[k] = sb[k][t];
+            const double c = pc_cost(a[r], bb, p.d, p.cmax);
+            e[q] = __dadd_rn(__dmul_rn(p.ng, c), scp[t]);
+            if (p.rowpot) e[q] = __dadd_rn(e[q], rp[r]);
+          } else {
+            e[q] = OTN_NINF;
+          }
+          cm = fmax(cm, e[q]);
+        }
+        if (cm > m[r]) {
+          s[r] = s[r] * exp_fast(m[r] - cm);
+          m[r] = cm;
+        }
+        if (m[r] != OTN_NINF) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) s[r] += exp_fast(e[q] - m[r]);
+        }
+      }
+    } else {
+      for (int t = lane; t < jn; t += 32) {
+        double bb[kPcMaxDim];
+#pragma unroll
+        for (int k = 0; k < kPcMaxDim; ++k) bb[k] = sb[k][t];
+        const double cpj = scp[t], vj = svec[t];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+          const double c = pc_cost(a[r], bb, p.d, p.cmax);
+          if (OP == OTN_PC_MAXD) {
+            m[r] = fmax(m[r], c);
+          } else if (OP == OTN_PC_CDOT) {
+            s[r] = fma(c, vj, s[r]);
+          } else {
+            const double kc = __dmul_rn(p.ng, c);
+            const double e = p.order == 0 ? __dadd_rn(__dadd_rn(kc, cpj), rp[r])
+                                          : __dadd_rn(__dadd_rn(kc, rp[r]), cpj);
+            const double pe = exp_fast(e);
+            if (OP == OTN_PC_DOT) {
+              s[r] = fma(pe, vj, s[r]);
+            } else if (OP == OTN_PC_DOTC) {
+              s[r] = fma(__dmul_rn(pe, c), vj, s[r]);
+            } else {  // DIAG: sum P^2 vec, max exponent
+              s[r] = fma(__dmul_rn(pe, pe), vj, s[r]);
+              m[r] = fmax(m[r], e);
+            }
+          }
+        }
+      }
+    }
+  }
+  // per-row warp reduction (fixed tree), lane 0 writes
+#pragma unroll
+  for (int r = 0; r < RW; ++r) {
+    const int64_t i = i0 + r;
+    double mm = m[r], ss = s[r];
+    if (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART) {
+      warp_lse(mm, ss);
+    } else {
+      if (OP == OTN_PC_MAXD || OP == OTN_PC_DIAG) mm = warp_max(mm);
+      if (OP != OTN_PC_MAXD) ss = warp_sum(ss);
+    }
+    if (lane == 0 && i < p.na) {
+      if (OP == OTN_PC_LSE) {
+        const double lse = lse_value(mm, ss);
+        double o = 0.0;
+        if (p.outer) {
+          o = __ldg(p.outer + i);
+          if (p.outer_d) o = __dadd_rn(o, __dmul_rn(p.alpha, __ldg(p.outer_d + i)));
+        }
+        p.out[i] = p.mode == 0 ? __dadd_rn(o, lse) : __dsub_rn(o, lse);
+      } else if (OP == OTN_PC_LSE_PART) {
+        p.out[i] = mm;
+        p.out2[i] = ss;
+      } else if (OP == OTN_PC_MAXD) {
+        p.out[i] = mm;
+      } else {
+        p.out[i] = ss;
+        if (OP == OTN_PC_DIAG && p.out2) p.out2[i] = mm;
+      }
+    }
+  }
+}
+
+template <int OP>
+static cudaError_t launch_pair_op(const PairArgs& p, cudaStream_t st, int num_sms) {
+  // fewer rows per warp when the row count cannot fill the machine twice
+  const int64_t ctas8 = (p.na + 63) / 64;
+  if (ctas8 >= 2 * num_sms) {
+    k_pair<8, OP><<<unsigned(ctas8), kPcThreads, 0, st>>>(p);
+  } else {
+    k_pair<2, OP><<<unsigned((p.na + 15) / 16), kPcThreads, 0, st>>>(p);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pair(otn_ctx* x, const PairArgs& p) {
+  switch (p.op) {
+    case OTN_PC_LSE: return launch_pair_op<OTN_PC_LSE>(p, x->stream, x->num_sms);
+    case OTN_PC_DOT: return launch_pair_op<OTN_PC_DOT>(p, x->stream, x->num_sms);
+    case OTN_PC_DIAG: return launch_pair_op<OTN_PC_DIAG>(p, x->stream, x->num_sms);
+    case OTN_PC_MAXD: return launch_pair_op<OTN_PC_MAXD>(p, x->stream, x->num_sms);
+    case OTN_PC_LSE_PART: return launch_pair_op<OTN_PC_LSE_PART>(p, x->stream, x->num_sms);
+    case OTN_PC_DOTC: return launch_pair_op<OTN_PC_DOTC>(p, x->stream, x->num_sms);
+    case OTN_PC_CDOT: return launch_pair_op<OTN_PC_CDOT>(p, x->stream, x->num_sms);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace otn

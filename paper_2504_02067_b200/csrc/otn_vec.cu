@@ -22,6 +22,18 @@ __global__ void k_vec(int op, int64_t n, double s, const double* a, const double
       case OTN_VEC_EXTRAP: o = __dadd_rn(a[i], __dmul_rn(s, __dsub_rn(a[i], b[i]))); break;
       case OTN_VEC_EXP: o = exp_fast(a[i]); break;
       case OTN_VEC_GRAD: o = __dsub_rn(exp_fast(a[i]), b[i]); break;
+      case OTN_VEC_MUL_SUB: o = __dsub_rn(__dmul_rn(a[i], b[i]), __dmul_rn(s, c[i])); break;
+      case OTN_VEC_DIV: o = __ddiv_rn(a[i], b[i]); break;
+      case OTN_VEC_SUB: o = __dsub_rn(a[i], b[i]); break;
+      case OTN_VEC_ADD: o = __dadd_rn(a[i], b[i]); break;
+      case OTN_VEC_PRECOND: o = __dmul_rn(a[i], __dsub_rn(1.0, __dmul_rn(s, b[i]))); break;
+      case OTN_VEC_NEG_DIV: o = __ddiv_rn(-a[i], b[i]); break;
+      case OTN_VEC_RESCALE: o = __dmul_rn(a[i], exp_fast(__dsub_rn(b[i], c[i]))); break;
+      case OTN_VEC_LSE_FIN: o = __dadd_rn(a[i], lse_value(b[i], c[i])); break;
+      case OTN_VEC_LSE_FIN_SUB: o = __dsub_rn(a[i], lse_value(b[i], c[i])); break;
+      case OTN_VEC_ROUND_SCALE: o = b[i] > 0.0 ? fmin(1.0, __ddiv_rn(a[i], b[i])) : 1.0; break;
+      case OTN_VEC_SUB_MUL: o = __dsub_rn(a[i], __dmul_rn(b[i], c[i])); break;
+      case OTN_VEC_MUL: o = __dmul_rn(a[i], b[i]); break;
       default: o = 0.0;
     }
     out[i] = o;
@@ -54,8 +66,17 @@ __global__ void __launch_bounds__(1024) k_reduce(int op, int64_t n, const double
       case OTN_RED_SUM_EXP: s0 += exp_fast(a[i]); break;
       case OTN_RED_DOT: s0 = fma(a[i], b[i], s0); break;
       case OTN_RED_L1: s0 += fabs(a[i]); break;
+      case OTN_RED_L1_ADD: s0 += fabs(__dadd_rn(a[i], b[i])); break;
+      case OTN_RED_NONPOS: if (a[i] <= 0.0) s0 += 1.0; break;
+      case OTN_RED_L1_DOT: s0 += fabs(a[i]); s1 = fma(a[i], b[i], s1); break;
+      case OTN_RED_MAX: s1 = (i == threadIdx.x) ? a[i] : fmax(s1, a[i]); break;
       default: break;
     }
+  }
+  if (op == OTN_RED_MAX) {
+    const double mx = block_max(n > threadIdx.x ? s1 : OTN_NINF, sh);
+    if (threadIdx.x == 0) { dst[0] = mx; dst[1] = 0.0; }
+    return;
   }
   s0 = block_sum(s0, sh);
   s1 = block_sum(s1, sh);

@@ -350,6 +350,62 @@ class DualState:
             self.u = np.asarray(z[:n], dtype=np.float64)
             self.v = np.asarray(z[n:], dtype=np.float64)
 
-    def _z_dev(self):
+    # -- hooks used by project() / mdot() (shared with the point-cloud state) ---
+    def _row_scaling_update(self):
+        """u = (u + log r) - log r(P)  (projector.py:146, dual.py:189)."""
+        self._ctx.call("otn_vec", _lib.VEC_ADD_SUB, 0.0, vptr(self._u), vptr(self._log_r),
+                       vptr(self._lr_dev()), None, vptr(self._u))
+        self._invalidate()
+
+    def _accept(self, alpha, d_u, d_v):
+        """u += alpha d_u; v = (v + alpha d_v) + (log c - trial); log c(P) = log c
+        (projector.py:234-236)."""
+        k = self._ctx
+        k.call("otn_vec", _lib.VEC_AXPY, float(alpha), vptr(self._u), vptr(d_u), None, None,
+               vptr(self._u))
+        k.call("otn_vec", _lib.VEC_STEP_V, float(alpha), vptr(self._v), vptr(d_v),
+               vptr(self._log_c), vptr(self._trial_vec), vptr(self._v))
+        self._invalidate()
+        self._lc.copy_(self._log_c)
+
+    def _system(self):
+        from .newton import DiscountedSystem
+        return DiscountedSystem.from_state(self)
+
+    def _dir_bufs(self):
+        bufs = getattr(self, "_dirbufs", None)
+        if bufs is None:
+            bufs = (self._ctx.vec(), self._ctx.vec())
+            self._dirbufs = bufs
+        return bufs
+
+    def _download_rows(self, buf):
+        return self._ctx.download(buf)
+
+    def _snapshot(self):
         """Device copy of (u, v) for the annealing driver's extrapolation."""
         return self._u.clone(), self._v.clone()
+
+    def _extrapolate(self, step, z_cur, z_prev):
+        """(u, v) = z + step * (z - z_prev)  (driver.py:170-175)."""
+        k = self._ctx
+        k.call("otn_vec", _lib.VEC_EXTRAP, float(step), vptr(z_cur[0]), vptr(z_prev[0]), None,
+               None, vptr(self._u))
+        k.call("otn_vec", _lib.VEC_EXTRAP, float(step), vptr(z_cur[1]), vptr(z_prev[1]), None,
+               None, vptr(self._v))
+        self._invalidate()
+
+    def _finalize(self, problem):
+        """Fresh plan, rounding onto U(r, c), primal <P, C> (driver.py:306-310).
+        Returns (P in the problem's array type, primal cost)."""
+        from ._device import TELEMETRY
+        from .driver import _round_device
+        k = self._ctx
+        P, _ = self._materialize(reuse_buffer=True)
+        primal = _round_device(k, P, self._dc.C, k.vec(problem.r), k.vec(problem.c))
+        opcount.add(1)          # <P, C>  (driver.py:309)
+        if is_tensor(problem.C):
+            return P[:, : problem.n], primal
+        out = P[:, : problem.n].cpu().numpy()
+        TELEMETRY.d2h += out.nbytes
+        return out, primal

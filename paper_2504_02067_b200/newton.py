@@ -153,6 +153,13 @@ class DiscountedSystem:
                        vptr(self._cP), float(rho), vptr(self._in(d)), vptr(out))
         return _as_host(d, out, self._ctx)
 
+    def _newton_dir(self, grad_u, eta, rho0, zero_init, max_cg_iters, d_u, d_v):
+        """newton_solve + d_v = -apply_pc(d_u) + slope in one device launch
+        (newton.py:175-210, projector.py:196-205); op tally included."""
+        res = _newton_device(grad_u, self, eta, rho0, zero_init, max_cg_iters, d_u, d_v)
+        opcount.add(1)                       # d_v = -apply_pc(d_u)  (projector.py:201)
+        return res
+
     def _tally_mu(self):
         if not self._mu_counted:
             opcount.add(2)

@@ -1,0 +1,65 @@
+"""On-the-fly point-cloud path (D4/D5 kernels) on the B200: the cost recomputed
+from coordinates must reproduce the stored-cost path and the reference."""
+
+import numpy as np
+import pytest
+
+from conftest import load_traj
+from paper_2504_02067_b200 import DualState, mdot, opcount, problems
+from paper_2504_02067_b200.pointcloud import PointCloudCost, PointCloudState
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(n, d, seed):
+    pc = problems.points_problem(n, d, seed)
+    dense = problems.Problem(C=pc.materialize_cost(), r=pc.r, c=pc.c)
+    return pc, dense
+
+
+@pytest.mark.parametrize("n,d", [(300, 2), (257, 3), (1024, 3)])
+def test_otf_lse_and_plan_match_stored(n, d):
+    import torch
+    pc, dense = _pair(n, d, 5)
+    cost = PointCloudCost(pc, torch.device("cuda", 0))
+    assert cost.cmax == pc.raw_cost_rows(0, n).max()
+    rng = np.random.default_rng(1)
+    u = np.log(pc.r) + 0.3 * rng.standard_normal(n)
+    v = np.log(pc.c) + 0.3 * rng.standard_normal(n)
+    gamma = 40.0
+    a = PointCloudState(cost, gamma, u, v, pc.r, pc.c)
+    b = DualState(dense, gamma, u=u, v=v)
+    a.refresh()
+    np.testing.assert_allclose(a._lr.cpu().numpy(), b.log_rP, rtol=1e-13)
+    np.testing.assert_allclose(a._lc.cpu().numpy(), b.log_cP, rtol=1e-13)
+    sa, sb = a._system(), b._system()
+    np.testing.assert_allclose(sa._mu.cpu().numpy(), sb.diag_prc(), rtol=1e-12)
+    x = torch.from_numpy(rng.standard_normal(n)).cuda()
+    from paper_2504_02067_b200.pointcloud import _Result
+    qa = cost.zeros(n)
+    sa._hvp(0.9, x, qa, _Result())
+    qb = sb.apply_F(0.9, x.cpu().numpy())
+    np.testing.assert_allclose(qa.cpu().numpy(), qb, rtol=1e-11, atol=1e-15)
+
+
+@pytest.mark.parametrize("name", ["pts256_2d_s0", "pts1024_2d_s0_fixed", "pts1024_3d_s0"])
+def test_otf_mdot_matches_reference_trajectory(name):
+    """Strict gate: same stages / Newton steps / CG counts / op
+    tally as the reference on the materialized cost, potentials to 1e-10."""
+    meta, arr = load_traj(name)
+    _, n, d, seed = meta["spec"].split(":")
+    pc = problems.points_problem(int(n), int(d), int(seed))
+    opcount.reset()
+    sol = mdot(pc, meta["gamma_i"], meta["gamma_f"])
+    assert [it.stats.cg_iters for it in sol.iterations] == [s["cg_iters"] for s in meta["stages"]]
+    assert [it.stats.newton_steps for it in sol.iterations] == \
+        [s["newton_steps"] for s in meta["stages"]]
+    assert sol.report.ops == meta["ops"]
+    st = sol.final_state
+    du = np.abs(st.u - arr["u"]).max() / np.abs(arr["u"]).max()
+    dv = np.abs(st.v - arr["v"]).max() / np.abs(arr["v"]).max()
+    assert du <= 1e-10 and dv <= 1e-10, (du, dv)
+    assert sol.P is None
+    assert sol.primal_cost == pytest.approx(meta["primal"], rel=1e-9)
+    st.set_targets(pc.r, pc.c)
+    assert st.grad_norm_l1() <= 2 * meta["true_marginal_err"] + 1e-12
