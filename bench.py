@@ -23,9 +23,12 @@ primal cost).  The metric is seconds per solve (lower is better).
          same n = 4096 problem, scaled by the reference's own primitive-call
          counts for this solve (tests/golden/callmix_*.json).
 
-Multi-GPU (--gpus N under torchrun): replicas only — the n = 4096 solve does
-not shard profitably; each rank solves its own seed, value is the
-max-over-ranks time per solve divided by N (whole-job seconds per solve).
+Multi-GPU (--gpus N under torchrun): the headline n = 4096 solve runs as
+replicas (it does not shard profitably): each rank solves its own
+seed, value is the max-over-ranks time per solve divided by N.  The sharded
+path is measured in ``extras.d4``: D4 (n = 65536 3-D points, on-the-fly cost)
+row-sharded over all N ranks, with one NCCL allreduce per column-direction
+product (max-over-ranks wall time).  ``extras`` also times D1 and D3 at N = 1.
 """
 
 from __future__ import annotations
@@ -35,7 +38,6 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 
 import numpy as np
@@ -62,55 +64,56 @@ def peaks():
 # clocks during the timed region (NVML)
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    REASONS = {
-        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
-        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
-        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
-        0x100: "display_clock_setting",
-    }
+    """nvidia-smi in a SUBPROCESS (no GIL contention with the solver's host
+    loop) sampling SM clocks and throttle reasons every 200 ms."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
-        self.samples, self.reasons, self.ok = [], set(), False
-        self.max_mhz = None
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self.ok = True
-        except Exception:
-            pass
-        self._stop = threading.Event()
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.05)
+        self.index = index
+        self.proc = None
+        self.lines = []
 
     def __enter__(self):
-        if self.ok:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+        import subprocess
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        if self.ok:
-            self.t.join()
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
-        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        clk, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            try:
+                clk.append(float(parts[0]))
+                mx = float(parts[1])
+            except (ValueError, IndexError):
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not clk:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["nvidia-smi unavailable"]}
+        return {"sm_mhz": float(statistics.median(clk)), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(clk)}
 
 
 # ---------------------------------------------------------------------------
@@ -127,6 +130,10 @@ def run_ours(args, rank, world):
     seed = rank  # replicas: one seed per rank
     host_prob = ot.workload(WORKLOAD["spec"].format(seed=seed))
     n = host_prob.n
+    # e2e inputs come from page-locked host memory (the contract's H2D source)
+    pinned_C = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    pinned_C.numpy()[:] = host_prob.C
+    host_prob = ot.Problem(C=pinned_C.numpy(), r=host_prob.r, c=host_prob.c, label=host_prob.label)
     dprob = ot.Problem(C=torch.from_numpy(host_prob.C).to(dev), r=host_prob.r, c=host_prob.c,
                        label=host_prob.label)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
@@ -152,10 +159,12 @@ def run_ours(args, rank, world):
             flush.fill_(1.0)                         # evict L2 between steps (untimed)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            sols.append(solve(dprob))
+            sol = solve(dprob)
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
+            del sol                                  # a held result would pin a 134 MB plan
+                                                     # buffer and force fresh allocations
         torch.cuda.synchronize()
     TELEMETRY.time_coop = False
     launches = TELEMETRY.launches
@@ -164,6 +173,8 @@ def run_ours(args, rank, world):
     barrier(world)
 
     # ---- e2e through the public API with host buffers ------------------------
+    _warm = solve(host_prob)              # warm the page-locked result buffer (untimed)
+    del _warm
     TELEMETRY.reset()
     e2e_ms = []
     for _ in range(args.steps):
@@ -173,10 +184,13 @@ def run_ours(args, rank, world):
         sol_h = solve(host_prob)          # H2D of C inside, D2H of the rounded P inside
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        if len(e2e_ms) < args.steps:
+            del sol_h
     h2d = TELEMETRY.h2d / args.steps
     d2h = TELEMETRY.d2h / args.steps
 
     # ---- precision check of the timed solves (after the timed region) -----
+    sols.append(solve(dprob))             # one more (untimed) solve for the precision check
     errs = []
     for s in sols[:1] + [sol_h]:
         st = s.final_state
@@ -233,9 +247,83 @@ def run_ours(args, rank, world):
         "e2e_per_step_ms": e2e_ms,
         "calls_per_step": {k: v / args.steps for k, v in calls.items()},
     }
+    if not args.no_extras:
+        out["extras"] = run_extras(args, rank, world, dev)
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(host_prob, budget_s=args.cpu_budget)
     return out
+
+
+# FP64-pipe instructions per plan entry in the on-the-fly pair kernel (counted
+# from the SASS of k_pair<8, DOT>: ~25 DFMA + ~17 DADD + ~8 DMUL per entry).
+PAIR_FP64_INSTR_PER_ENTRY = 50
+
+
+def run_extras(args, rank, world, dev):
+    """The other BASELINE configurations, one timed solve each (after a warm-up):
+    D1 (n=1024 2-D points, fixed gamma), D3 (n=4096 784-d pixel sets, stored C),
+    and D4 (n=65536 3-D points, on-the-fly cost) — row-sharded over all ranks
+    with NCCL allreduces when launched with --gpus N > 1."""
+    import torch
+
+    import paper_2504_02067_b200 as ot
+    from paper_2504_02067_b200._device import TELEMETRY
+    from paper_2504_02067_b200.pointcloud import Comm, PointCloudCost
+    extras = {}
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        res = fn()
+        torch.cuda.synchronize()
+        return res, max_over_ranks(time.perf_counter() - t0, world)
+
+    try:
+        if world == 1:
+            for key, spec, gi, gf in (("d1_fixed", "pts:1024:2:0", 2.0 ** 10, 2.0 ** 10),
+                                      ("d3", "pix:4096:784:0", 2.0 ** 5, 2.0 ** 16)):
+                p = ot.workload(spec)
+                dp = ot.Problem(C=torch.from_numpy(p.C).to(dev), r=p.r, c=p.c)
+                ot.mdot(dp, gi, gf)
+                sol, dt = timed(lambda: ot.mdot(dp, gi, gf))
+                st = sol.final_state
+                st.set_targets(p.r, p.c)
+                extras[key] = {"spec": spec, "gamma": [gi, gf], "s": dt,
+                               "stages": len(sol.iterations),
+                               "cg": sum(i.stats.cg_iters for i in sol.iterations),
+                               "true_marginal_err": st.grad_norm_l1()}
+        n4 = args.d4_n
+        pc = ot.points_problem(n4, 3, 0)
+        comm = Comm()
+
+        def d4():
+            cost = PointCloudCost(pc, dev, comm=comm)
+            return ot.mdot(pc, 2.0 ** 5, 2.0 ** 10, cost=cost)
+        if args.d4_warmup:
+            d4()
+        TELEMETRY.reset()
+        sol, dt = timed(d4)
+        passes = TELEMETRY.calls.get("otn_pc_pass", 0)
+        st = sol.final_state
+        st.set_targets(pc.r, pc.c)
+        err = st.grad_norm_l1()
+        entries = float(n4) * n4 * passes / world     # per rank (each pass covers n x n/world)
+        clk = 1.965e9
+        peak_entries = 148 * 64 * clk / PAIR_FP64_INSTR_PER_ENTRY
+        extras["d4"] = {"n": n4, "dim": 3, "gamma": [2.0 ** 5, 2.0 ** 10], "gpus": world,
+                        "sharding": "rows" if world > 1 else "none", "s": dt,
+                        "stages": len(sol.iterations),
+                        "cg": sum(i.stats.cg_iters for i in sol.iterations),
+                        "passes_per_rank": passes, "true_marginal_err": err,
+                        "primal": sol.primal_cost,
+                        "entries_per_s_per_gpu": entries / dt,
+                        "fp64_pipe_frac_est": entries / dt / peak_entries,
+                        "fp64_basis": f"{PAIR_FP64_INSTR_PER_ENTRY} FP64 instr/entry (SASS), "
+                                      "64 FP64 instr/clk/SM x 148 SMs x 1.965 GHz"}
+    except Exception as exc:                      # extras never break the headline line
+        extras["error"] = f"{type(exc).__name__}: {exc}"
+    return extras
 
 
 # ---------------------------------------------------------------------------
@@ -357,6 +445,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--d4-n", type=int, default=65536)
+    ap.add_argument("--d4-warmup", type=int, default=0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     rank, world = init_dist(args)

@@ -406,6 +406,10 @@ class DualState:
         opcount.add(1)          # <P, C>  (driver.py:309)
         if is_tensor(problem.C):
             return P[:, : problem.n], primal
-        out = P[:, : problem.n].cpu().numpy()
-        TELEMETRY.d2h += out.nbytes
-        return out, primal
+        # D2H through page-locked memory (DMA at full PCIe/C2C rate; a pageable
+        # copy of the 134 MB plan is ~25x slower); torch caches the pinned block
+        t = torch()
+        host = t.empty((problem.n, problem.n), dtype=t.float64, pin_memory=True)
+        host.copy_(P[:, : problem.n])
+        TELEMETRY.d2h += host.numel() * 8
+        return host.numpy(), primal

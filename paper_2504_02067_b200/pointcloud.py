@@ -88,26 +88,57 @@ class Comm:
         return [float(v) for v in t.tolist()]
 
 
-class PointCloudCost:
-    """Device-resident point sets of a (possibly row-sharded) point-cloud problem."""
+class CudaBackend:
+    """The C-ABI pair / vector / reduction kernels on one CUDA device."""
 
-    def __init__(self, problem, device, comm=None):
-        t = torch()
+    def __init__(self, device):
+        self.device = device
+        self.ctx = Context.get(32, device)        # stream + scalar plumbing only
+
+    def pass_(self, op, A, na, B, nb, d, cmax, ng, order, colpot, colpot_d, alpha, rowpot, vec,
+              outer, outer_d, mode, out, out2):
+        self.ctx.call("otn_pc_pass", int(op), vptr(A), int(na), int(na), vptr(B), int(nb),
+                      int(nb), int(d), float(cmax), float(ng), int(order), vptr(colpot),
+                      vptr(colpot_d), float(alpha), vptr(rowpot), vptr(vec), vptr(outer),
+                      vptr(outer_d), int(mode), vptr(out), vptr(out2))
+
+    def vec(self, n, op, out, a, b=None, c=None, d=None, s=0.0):
+        self.ctx.call("otn_vec_n", int(n), int(op), float(s), vptr(a), vptr(b), vptr(c), vptr(d),
+                      vptr(out))
+
+    def reduce(self, n, op, a, b=None, c=None, d=None):
+        out = (ctypes.c_double * 2)()
+        fl = ctypes.c_int(0)
+        self.ctx.call("otn_reduce_n", int(n), int(op), vptr(a), vptr(b), vptr(c), vptr(d), out,
+                      ctypes.byref(fl))
+        return float(out[0]), float(out[1]), int(fl.value)
+
+    def tensor(self, arr):
+        TELEMETRY.h2d += arr.nbytes
+        return torch().from_numpy(arr.copy()).to(self.device)
+
+
+class PointCloudCost:
+    """Device-resident point sets of a (possibly row-sharded) point-cloud problem.
+
+    ``backend`` executes the O(n^2) passes and vector kernels (the CUDA C-ABI;
+    tests inject a CPU double to exercise the sharding logic under gloo)."""
+
+    def __init__(self, problem, device, comm=None, backend=None):
         self.problem = problem
         self.comm = comm or Comm()
         self.device = device
+        self.be = backend or CudaBackend(device)
         self.n = problem.n
         self.d = problem.dim
         if not 1 <= self.d <= 4:
             raise DomainError("on-the-fly cost supports point dimension 1..4")
         self.row0, self.row1 = self.comm.shard(self.n)
         self.rows = self.row1 - self.row0
-        self.ctx = Context.get(32, device)        # stream + scalar plumbing only
         X = np.ascontiguousarray(problem.X[self.row0:self.row1].T)   # SoA: d x rows
         Y = np.ascontiguousarray(problem.Y.T)                        # SoA: d x n
-        self.Xt = t.from_numpy(X).to(device)
-        self.Yt = t.from_numpy(Y).to(device)
-        TELEMETRY.h2d += X.nbytes + Y.nbytes
+        self.Xt = self.be.tensor(X)
+        self.Yt = self.be.tensor(Y)
         self.symmetric = bool(np.array_equal(problem.X, problem.Y))
         if problem.cmax is not None:
             self.cmax = float(problem.cmax)
@@ -124,7 +155,7 @@ class PointCloudCost:
         local = self.reduce(self.rows, _lib.RED_MAX, per_row)[0]
         return self.comm.max_scalars([local], self.device)[0]
 
-    # ---- thin wrappers over the C-ABI ------------------------------------------
+    # ---- thin wrappers over the backend ----------------------------------------
     def pass_(self, op, rows_first, out, ng=0.0, order=0, colpot=None, colpot_d=None, alpha=0.0,
               rowpot=None, vec=None, outer=None, outer_d=None, mode=0, out2=None, cmax=None):
         """rows_first: A = own X rows, B = all Y (row pass); else A = Y, B = own X."""
@@ -132,30 +163,21 @@ class PointCloudCost:
             A, na, B, nb = self.Xt, self.rows, self.Yt, self.n
         else:
             A, na, B, nb = self.Yt, self.n, self.Xt, self.rows
-        self.ctx.call("otn_pc_pass", int(op), vptr(A), int(na), int(na), vptr(B), int(nb),
-                      int(nb), int(self.d), float(self.cmax if cmax is None else cmax), float(ng),
-                      int(order), vptr(colpot), vptr(colpot_d), float(alpha), vptr(rowpot),
-                      vptr(vec), vptr(outer), vptr(outer_d), int(mode), vptr(out), vptr(out2))
+        self.be.pass_(op, A, na, B, nb, self.d, self.cmax if cmax is None else cmax, ng, order,
+                      colpot, colpot_d, alpha, rowpot, vec, outer, outer_d, mode, out, out2)
 
     def vec(self, n, op, out, a, b=None, c=None, d=None, s=0.0):
-        self.ctx.call("otn_vec_n", int(n), int(op), float(s), vptr(a), vptr(b), vptr(c), vptr(d),
-                      vptr(out))
+        self.be.vec(n, op, out, a, b, c, d, s)
 
     def reduce(self, n, op, a, b=None, c=None, d=None):
-        out = (ctypes.c_double * 2)()
-        fl = ctypes.c_int(0)
-        self.ctx.call("otn_reduce_n", int(n), int(op), vptr(a), vptr(b), vptr(c), vptr(d), out,
-                      ctypes.byref(fl))
-        return float(out[0]), float(out[1]), int(fl.value)
+        return self.be.reduce(n, op, a, b, c, d)
 
     def zeros(self, n):
         t = torch()
         return t.zeros(n, dtype=t.float64, device=self.device)
 
     def upload(self, values):
-        arr = np.ascontiguousarray(values, dtype=np.float64)
-        TELEMETRY.h2d += arr.nbytes
-        return torch().from_numpy(arr.copy()).to(self.device)
+        return self.be.tensor(np.ascontiguousarray(values, dtype=np.float64))
 
     # ---- column-direction log-sum-exp (all rows, across shards) ----------------
     def lse_cols(self, ng, inner, inner_d, alpha, outer, outer_d, mode, out):
@@ -419,7 +441,7 @@ class PointCloudState:
         lo, hi = pc.row0, pc.row1
         self._touch_K()
         opcount.add(4)                                  # materialize (dual.py:163)
-        ones = t.ones(n, dtype=t.float64, device=pc.device)
+        ones = pc.upload(np.ones(n))
         rsum = pc.zeros(nr)
         pc.pass_(_lib.PC_DOT, rows_first=True, out=rsum, ng=self._ng, colpot=self._v,
                  rowpot=self._u, vec=ones)
@@ -446,8 +468,8 @@ class PointCloudState:
         err_c = pc.zeros(n)
         pc.vec(n, _lib.VEC_SUB_MUL, err_c, c_all, cs, csum)            # driver.py:202
         opcount.add(1)
-        deficit = pc.comm.sum_scalars([pc.reduce(nr, _lib.RED_DOT, err_r, t.ones(
-            nr, dtype=t.float64, device=pc.device))[0]], pc.device)[0]
+        deficit = pc.comm.sum_scalars([pc.reduce(nr, _lib.RED_DOT, err_r,
+                                                 pc.upload(np.ones(nr)))[0]], pc.device)[0]
         # <P, C> = sum_i rs_i sum_j P_ij C_ij cs_j (+ rank-one term)
         tcost = pc.zeros(nr)
         pc.pass_(_lib.PC_DOTC, rows_first=True, out=tcost, ng=self._ng, colpot=self._v,
@@ -496,8 +518,7 @@ class PointCloudSystem:
         self._icP = pc.zeros(n)
         pc.vec(nr, _lib.VEC_EXP, self._rP, state._lr_dev())
         pc.vec(n, _lib.VEC_EXP, self._cP, state._lc_dev())
-        ones = torch().ones(n, dtype=torch().float64, device=pc.device)
-        pc.vec(n, _lib.VEC_DIV, self._icP, ones, self._cP)
+        pc.vec(n, _lib.VEC_DIV, self._icP, pc.upload(np.ones(n)), self._cP)
         # Jacobi diagonal + the materialize overflow check in one pass
         sq = pc.zeros(nr)
         emax = pc.zeros(nr)
