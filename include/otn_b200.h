@@ -118,6 +118,11 @@ int otn_destroy(otn_ctx* ctx);
 int otn_set_stream(otn_ctx* ctx, void* stream);
 /* out4 = {n, ld, persistent-solver CTAs, workspace bytes} */
 int otn_info(const otn_ctx* ctx, int64_t* out4);
+/* Synchronize and copy the row partition and plan mode of the last
+ * persistent-solver launch: host[0..G] = row boundaries of the G CTAs,
+ * host[G+1] = plan mode (0 streamed ring, 1 L2-resident direct, 2 sparse
+ * shared-memory rows); G = otn_info()[2].  Diagnostic (bench / tests).     */
+int otn_coop_layout(otn_ctx* ctx, int* host);
 /* Synchronize and copy the four device status flags to the host:
  * [0] plan overflow, [1] nonpositive sums, [2] reduce domain, [3] rounding. */
 int otn_read_flags(otn_ctx* ctx, int* host4);
@@ -145,12 +150,13 @@ int otn_trial_cols(otn_ctx* ctx, const double* C, int symmetric, double neg_gamm
 
 /* ---- plan (K4 + K5) ------------------------------------------------------ */
 /* A plan is the pair (P, seg_mask).  seg_mask (nullable = dense) holds one bit
- * per 64-column (512-byte) row segment, set iff the segment has a nonzero:
- * n rows x OTN_MASK_WORDS(ld) uint64 words, bit s%64 of word s/64 for segment
- * s.  The Hessian-vector kernels skip all-zero segments (exp underflow makes
- * most of the plan exactly 0 at weak regularization); skipped terms are exact
- * zeros, so results are identical to the dense computation.                 */
-#define OTN_MASK_WORDS(ld) (((ld) + 4095) / 4096)
+ * per 64-column (512-byte) row segment, set iff the segment has a nonzero, and
+ * the row's nonzero count: n rows x OTN_MASK_WORDS(ld) uint64 words, bit s%64
+ * of word s/64 for segment s, then one count word.  The Hessian-vector
+ * kernels skip all-zero segments (exp underflow makes most of the plan
+ * exactly 0 at weak regularization) and, when the plan is sparse enough,
+ * compress each CTA's rows into shared memory; skipped terms are exact zeros.*/
+#define OTN_MASK_WORDS(ld) (((ld) + 4095) / 4096 + 1)
 /* P_ij = exp((neg_gamma*C_ij + v_j) + u_i), and seg_mask if non-NULL.  If
  * icP != NULL also mu_i = (sum_j P_ij^2 icP_j) / rP_i (the Jacobi diagonal,
  * K5 fused).  Overflow (an exponent > 700) sets a device flag that the next

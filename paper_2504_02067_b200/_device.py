@@ -167,7 +167,7 @@ class Context:
     def seg_mask(self):
         """Plan segment-occupancy mask (OTN_MASK_WORDS(ld) uint64 words per row)."""
         t = torch()
-        return t.zeros((self.n, (self.ld + 4095) // 4096), dtype=t.int64, device=self.device)
+        return t.zeros((self.n, (self.ld + 4095) // 4096 + 1), dtype=t.int64, device=self.device)
 
     # ---- thin call helpers -----------------------------------------------
     def call(self, name, *args):

@@ -20,7 +20,9 @@ from .errors import (
 )
 
 LIB_NAME = "libotn_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# OTN_LIB_AB: alternate build of the same library, for side-by-side kernel timing (tools/)
+LIB_PATH = os.environ.get("OTN_LIB_AB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                         LIB_NAME)
 
 OTN_OK = 0
 OTN_ERR_CUDA = 1
@@ -87,6 +89,7 @@ SIGNATURES = {
     "otn_newton": [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I, _I64, _P, _P,
                    ctypes.POINTER(SolveResult)],
     "otn_probe": [_P, _P, _P, _P, _P, _P, _P, _I, _I64],
+    "otn_coop_layout": [_P],
     "otn_pc_pass": [_P, _I, _P, _I64, _I64, _P, _I64, _I64, _I, _D, _D, _I, _P, _P, _D, _P, _P,
                     _P, _P, _I, _P, _P],
     "otn_vec_n": [_P, _I64, _I, _D, _P, _P, _P, _P, _P],

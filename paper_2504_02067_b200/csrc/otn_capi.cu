@@ -139,6 +139,7 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
   size_t o_sc = off; off += align_up(64 * sizeof(double), 256);
   size_t o_fl = off; off += align_up(16 * sizeof(int), 256);
   size_t o_res = off; off += align_up(sizeof(otn::DevResult), 256);
+  size_t o_part = off; off += align_up(size_t(x->coop_blocks + 2) * sizeof(int), 256);
   x->ws_bytes = off;
   e = cudaMalloc(&x->ws, off);
   if (e != cudaSuccess) { delete x; return fail(OTN_ERR_CUDA, "otn_create: cudaMalloc", e); }
@@ -159,6 +160,7 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
   x->scal = (double*)(base + o_sc);
   x->flags = (int*)(base + o_fl);
   x->dres = (otn::DevResult*)(base + o_res);
+  x->part = (int*)(base + o_part);
   e = cudaMallocHost((void**)&x->h_scal, 64 * sizeof(double));
   if (e == cudaSuccess) e = cudaMallocHost((void**)&x->h_flags, 16 * sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost((void**)&x->h_res, sizeof(otn::DevResult));
@@ -192,6 +194,11 @@ int otn_info(const otn_ctx* x, int64_t* out4) {
   out4[2] = x->coop_blocks;
   out4[3] = int64_t(x->ws_bytes);
   return OTN_OK;
+}
+
+int otn_coop_layout(otn_ctx* x, int* host) {
+  OTN_REQUIRE(x && host, "otn_coop_layout: NULL argument");
+  return sync_copy(x, host, x->part, size_t(x->coop_blocks + 2) * sizeof(int), "otn_coop_layout");
 }
 
 int otn_read_flags(otn_ctx* x, int* host4) {
@@ -298,7 +305,7 @@ int otn_square_matvec(otn_ctx* x, const double* P, const double* w, double* out)
 static otn::CoopArgs plan_args(otn_ctx* x, const double* P, const uint64_t* seg_mask) {
   otn::CoopArgs a = base_args(x, P);
   a.mask = seg_mask;
-  a.mw = (x->ld + otn::kSegWordCols - 1) / otn::kSegWordCols;
+  a.mw = OTN_MASK_WORDS(x->ld);
   return a;
 }
 

@@ -31,7 +31,6 @@ constexpr int NT = kCoopThreads;
 constexpr int NW = NT / 32;         // warps per CTA
 constexpr int CH = 4;               // 16-byte chunks per thread per tile
 constexpr int TILE = NT * 2 * CH;   // 4096 columns
-constexpr int RB = 4;               // rows per phase-B group
 constexpr int kRows = 64;           // rows staged per chunk in phases A / B
 constexpr int kRefresh = 50;        // newton.py:38 TRUE_RESIDUAL_REFRESH
 constexpr int kMaxG = 256;          // grid-reduction fan-in handled in one pass
@@ -92,7 +91,7 @@ __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&v)[K]
 }
 
 // ---------------------------------------------------------------------------
-// Plan streaming: per-CTA column windows + per-thread cp.async rings.
+// Plan streaming: per-CTA column windows + register-staged direct loads.
 //
 // A work item is one row i of one 4096-column tile T of the plan; its span
 // [lo, hi) runs from the first to the last nonzero 64-column segment
@@ -102,18 +101,28 @@ __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&v)[K]
 // their union per tile — its column WINDOW — in shared memory.  Within a tile
 // thread t owns window columns {2t, 2t+1} + c*1024 (c < nch = ceil(W/1024)),
 // so for a sparse plan all threads work on the few nonzero columns instead of
-// most of them idling.  Each thread streams exactly its 16-byte chunks of each
-// row's span, kRingDepth-1 rows ahead, with cp.async (LDGSTS, L1-bypassing)
-// into its own ring slots and reads only what it copied: no barrier of any
-// kind inside a phase.  Chunks outside the span are exact zeros and are
-// neither loaded nor used: the results equal the dense computation bit for bit.
+// most of them idling.  Each thread loads its 16-byte chunks of U rows at once
+// (ld.global.cg, predicated on the span) before using them: the loads of a
+// batch are independent, so a warp keeps U * nch requests in flight with no
+// shared-memory staging and no barrier inside a phase.  (A per-thread
+// cp.async ring was measured 3-5x slower on L2-resident spans:
+// tools/l2stream.cu.)  Chunks outside the span are exact zeros and are neither
+// loaded nor used: the results equal the dense computation bit for bit.
 // ---------------------------------------------------------------------------
-constexpr int kRingDepth = 5;                       // rows per thread ring
 constexpr int kSpanSmem = 8192;                     // (row, tile) spans staged per CTA (32 KB)
 constexpr int kMaxTiles = 64;                       // ld <= 262144
 __shared__ uint32_t s_span[kSpanSmem];              // lo | hi << 16, relative to the tile
 __shared__ int s_win_lo[kMaxTiles], s_win_hi[kMaxTiles];
-extern __shared__ __align__(128) double2 s_ring[];  // [kRingDepth][CH][NT] double2
+// Plan mode of this launch (chosen by k_partition, uniform over the grid):
+//   kPlanRing    plan streamed from HBM through per-thread cp.async rings;
+//   kPlanL2      the masked plan (sum of row spans) fits in L2: register-
+//                batched direct loads;
+//   kPlanSparse  each CTA compresses its rows' nonzeros into shared memory
+//                once per launch (CSR for P w, a local CSC for P^T x).
+enum PlanMode { kPlanRing = 0, kPlanL2 = 1, kPlanSparse = 2 };
+__shared__ int s_mode;
+__shared__ int s_nzc;                               // kPlanSparse: nonempty columns of the CTA
+constexpr int64_t kL2ModeBytes = 80ll * 1024 * 1024;
 
 // Everything the streaming loops need, by value (registers, not the kernel's
 // parameter copy in local memory).
@@ -122,7 +131,15 @@ struct PlanView {
   const uint64_t* mask;     // global mask rows (nullptr = dense)
   int64_t ld, mw;
   int nt;                   // tiles
+  int mode;                 // PlanMode
 };
+
+// Plans too large for L2 (kPlanRing: streamed from HBM) use a per-thread
+// cp.async ring instead: kRingDepth rows of all CH chunks in flight, refilled
+// continuously (the register batches drain between batches, which costs HBM
+// bandwidth; on L2-resident spans the ring is the slower one).
+constexpr int kRingDepth = 5;
+extern __shared__ __align__(128) double2 s_ring[];  // [kRingDepth][CH][NT] double2
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -169,6 +186,7 @@ __device__ PlanView plan_view(const CoopArgs& a, int64_t r0, int64_t r1) {
   v.ld = a.ld;
   v.mw = a.mw;
   v.nt = ntiles_of(a.ld);
+  v.mode = s_mode;
   return v;
 }
 
@@ -198,10 +216,49 @@ __device__ void stage_layout(const CoopArgs& a, int64_t r0, int64_t r1, double* 
     if (rel < s_win_lo[ti] || rel >= s_win_hi[ti])
       *reinterpret_cast<double2*>(wrow + j) = make_double2(0.0, 0.0);
   }
+  __syncthreads();
 }
 
-// Issue this thread's chunks of row il into ring slot `slot` (smem byte
-// address `dst`), then commit one group (possibly empty).
+// Load this thread's chunks of one row (zeros outside the span).
+template <int NCH>
+__device__ __forceinline__ void load_row(const double* row, int lo, int hi, int col0,
+                                         double2 (&pv)[NCH]) {
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int col = col0 + c * NT * 2;
+    pv[c] = in_span(col, lo, hi) ? ldcg2(row + col) : make_double2(0.0, 0.0);
+  }
+}
+
+// Phase A over one tile, rows [c0, c0 + m) of the CTA: acc[c] += P_ij x_i
+// (rows ascending; a zero chunk leaves acc unchanged bit for bit).
+template <int NCH>
+__device__ __forceinline__ void phase_a_tile(const PlanView& v, const double* row0, int c0, int m,
+                                             int ti, int col0, double2 (&acc)[CH], const Smem& sh) {
+  constexpr int U = NCH <= 2 ? 8 : 4;
+  for (int q0 = 0; q0 < m; q0 += U) {
+    double2 pv[U][NCH];
+    double xi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int lo = 0, hi = 0;
+      if (q0 + u < m) get_span(v, c0 + q0 + u, ti, lo, hi);
+      xi[u] = sh.xs[q0 + u < m ? q0 + u : 0];
+      load_row<NCH>(row0 + int64_t(q0 + u) * v.ld, lo, hi, col0, pv[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        acc[c].x = fma(pv[u][c].x, xi[u], acc[c].x);
+        acc[c].y = fma(pv[u][c].y, xi[u], acc[c].y);
+      }
+    }
+  }
+}
+
+// Issue this thread's chunks of row il into the ring slot at smem byte
+// address `dst`, then commit one group (possibly empty).
 __device__ __forceinline__ void ring_fill(const PlanView& v, const double* src_row, int il, int ti,
                                           int col0, uint32_t dst) {
   int lo, hi;
@@ -214,18 +271,333 @@ __device__ __forceinline__ void ring_fill(const PlanView& v, const double* src_r
   cp_commit();
 }
 
+constexpr uint32_t kSlotBytes = CH * NT * 16;
+
+// Phase A over one wide tile through the ring (same sums as phase_a_tile).
+__device__ __forceinline__ void phase_a_ring(const PlanView& v, const double* fill_row, int c0,
+                                             int m, int ti, int col0, double2 (&acc)[CH],
+                                             const Smem& sh) {
+  const uint32_t ring0 = smem_u32(s_ring) + 16u * threadIdx.x;
+#pragma unroll
+  for (int d = 0; d < kRingDepth - 1; ++d) {
+    if (d < m) ring_fill(v, fill_row, c0 + d, ti, col0, ring0 + d * kSlotBytes);
+    else cp_commit();
+    fill_row += v.ld;
+  }
+  int slot = 0;
+  uint32_t fdst = ring0 + (kRingDepth - 1) * kSlotBytes;
+  for (int q = 0; q < m; ++q) {
+    if (q + kRingDepth - 1 < m) ring_fill(v, fill_row, c0 + q + kRingDepth - 1, ti, col0, fdst);
+    else cp_commit();
+    fill_row += v.ld;
+    fdst = fdst == ring0 + (kRingDepth - 1) * kSlotBytes ? ring0 : fdst + kSlotBytes;
+    cp_wait<kRingDepth - 1>();
+    int lo, hi;
+    get_span(v, c0 + q, ti, lo, hi);
+    const double xi = sh.xs[q];
+    const double2* row = s_ring + slot * CH * NT + threadIdx.x;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (in_span(col0 + c * NT * 2, lo, hi)) {
+        const double2 pv = row[c * NT];
+        acc[c].x = fma(pv.x, xi, acc[c].x);
+        acc[c].y = fma(pv.y, xi, acc[c].y);
+      }
+    }
+    slot = slot + 1 == kRingDepth ? 0 : slot + 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// kPlanSparse: compressed rows in shared memory.
+//
+// At weak regularization a row of the plan holds a few dozen nonzeros (the
+// rest underflow to exact 0), far fewer than its segment span.  Each CTA then
+// extracts its rows' nonzeros once per launch (warp per row, ballot
+// compaction, column order) into a CSR in the dynamic shared memory the ring
+// would otherwise use, plus a local CSC (a permutation sorted by column, rows
+// ascending within a column, built by a counting sort).  Phase A walks the
+// CSC: each column's partial is the rows-ascending fma chain of the dense
+// phase A, bit for bit.  Phase B walks the CSR, warp per row.
+// k_partition chooses this mode and a row partition balanced on nonzeros, and
+// guarantees the capacities below.
+// ---------------------------------------------------------------------------
+constexpr int kSparseRows = 512;                    // rows per CTA
+constexpr int kSparseCols = TILE;                   // one tile (ld <= 4096)
+constexpr int kSparseCap = 9200;                    // nonzeros per CTA
+constexpr size_t kSparseXs = 0;                     // double[kSparseCols]: x rows (A) / w window (B)
+constexpr size_t kSparseRp = kSparseXs + kSparseCols * 8;               // int[kSparseRows + 1]
+constexpr size_t kSparseCst = kSparseRp + (kSparseRows + 4) * 4;        // int[kSparseCols + 1]
+constexpr size_t kSparseVal = kSparseCst + (kSparseCols + 4) * 4;       // double[cap]
+constexpr size_t kSparseCol = kSparseVal + size_t(kSparseCap) * 8;      // u16[cap]
+constexpr size_t kSparseRow = kSparseCol + size_t(kSparseCap) * 2;      // u16[cap]
+constexpr size_t kSparsePerm = kSparseRow + size_t(kSparseCap) * 2;     // u16[cap]
+constexpr size_t kSparseBytes = kSparsePerm + size_t(kSparseCap) * 2;
+
+struct SparseView {
+  double* xs;
+  int* rp;
+  int* cst;
+  double* val;
+  uint16_t* col;
+  uint16_t* row;
+  uint16_t* perm;
+};
+
+__device__ __forceinline__ SparseView sparse_view() {
+  char* b = reinterpret_cast<char*>(s_ring);
+  return SparseView{reinterpret_cast<double*>(b + kSparseXs), reinterpret_cast<int*>(b + kSparseRp),
+                    reinterpret_cast<int*>(b + kSparseCst), reinterpret_cast<double*>(b + kSparseVal),
+                    reinterpret_cast<uint16_t*>(b + kSparseCol),
+                    reinterpret_cast<uint16_t*>(b + kSparseRow),
+                    reinterpret_cast<uint16_t*>(b + kSparsePerm)};
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+// In-place inclusive prefix sum of a[0, len), len <= NT * 8 (one CTA).
+__device__ void block_incl_scan(int* a, int len, Smem& sh) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int loc[8], sum = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = t * 8 + k;
+    sum += i < len ? a[i] : 0;
+    loc[k] = sum;
+  }
+  const int incl = warp_incl_scan(sum, lane);
+  int* wsum = reinterpret_cast<int*>(sh.red);         // 16 ints (free outside grid_reduce)
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int off = incl - sum;
+  for (int w = 0; w < warp; ++w) off += wsum[w];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = t * 8 + k;
+    if (i < len) a[i] = loc[k] + off;
+  }
+  __syncthreads();
+}
+
+// Extract this CTA's nonzeros (CSR, column order) and build the local CSC.
+__device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* wrow, Smem& sh) {
+  const SparseView sp = sparse_view();
+  const PlanView v = plan_view(a, r0, r1);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int rows = int(r1 - r0);
+  if (warp == 0) {                                  // row pointers from the mask count words
+    int run = 0;
+    for (int b = 0; b < rows; b += 32) {
+      const int r = b + lane;
+      const int c = r < rows ? int(__ldg(v.mask + (r0 + r) * v.mw + v.mw - 1)) : 0;
+      const int incl = warp_incl_scan(c, lane);
+      if (r < rows) sp.rp[r + 1] = run + incl;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) sp.rp[0] = 0;
+  }
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+  constexpr int U = 8;                              // 64-column steps loaded at once
+  for (int r = warp; r < rows; r += NW) {           // warp per row, columns ascending
+    int lo, hi;
+    get_span(v, r, 0, lo, hi);
+    const double* prow = v.P + (r0 + r) * v.ld;
+    int pos = sp.rp[r];
+    const int end = sp.rp[r + 1];
+    for (int j0 = lo; j0 < hi; j0 += 64 * U) {
+      double2 pv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + 64 * u + 2 * lane;
+        pv[u] = j < hi ? ldcg2(prow + j) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + 64 * u + 2 * lane;
+        const bool nx = pv[u].x != 0.0, ny = pv[u].y != 0.0;
+        const unsigned bx = __ballot_sync(0xffffffffu, nx), by = __ballot_sync(0xffffffffu, ny);
+        int q = pos + __popc(bx & lt) + __popc(by & lt);
+        if (nx) {
+          if (q < end) { sp.val[q] = pv[u].x; sp.col[q] = uint16_t(j); sp.row[q] = uint16_t(r); }
+          ++q;
+        }
+        if (ny && q < end) { sp.val[q] = pv[u].y; sp.col[q] = uint16_t(j + 1); sp.row[q] = uint16_t(r); }
+        pos += __popc(bx) + __popc(by);
+      }
+    }
+  }
+  const int ulo = s_win_lo[0], W = s_win_hi[0] - ulo;
+  for (int d = t; d <= W; d += NT) sp.cst[d] = 0;
+  __syncthreads();
+  const int E = sp.rp[rows];
+  for (int e = t; e < E; e += NT) atomicAdd(&sp.cst[sp.col[e] - ulo], 1);
+  __syncthreads();
+  block_incl_scan(sp.cst, W, sh);                   // cst[d] = end of column d
+  // place entries (slot order within a column is arbitrary here), ...
+  for (int e = t; e < E; e += NT) sp.perm[atomicSub(&sp.cst[sp.col[e] - ulo], 1) - 1] = uint16_t(e);
+  __syncthreads();
+  if (t == 0) sp.cst[W] = E;                        // cst[d] = start of column d
+  __syncthreads();
+  // ... then sort each column by entry index = by row (CSR is row-major):
+  // the rows-ascending order of the dense phase A, independent of the atomics.
+  for (int d = t; d < W; d += NT) {
+    const int k0 = sp.cst[d], k1 = sp.cst[d + 1];
+    for (int k = k0 + 1; k < k1; ++k) {
+      const uint16_t key = sp.perm[k];
+      int m = k - 1;
+      while (m >= k0 && sp.perm[m] > key) { sp.perm[m + 1] = sp.perm[m]; --m; }
+      sp.perm[m + 1] = key;
+    }
+  }
+  // Compact the nonempty columns in place of cst: cptr[m] (u16 start of the
+  // m-th nonempty column, cptr[nzc] = E) and ccol[m] (its window column).
+  int st[9], nonempty = 0;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const int d = t * 8 + k;
+    st[k] = d < W ? sp.cst[d] : E;
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) nonempty += st[k + 1] > st[k];
+  const int incl = warp_incl_scan(nonempty, lane);
+  int* wsum = reinterpret_cast<int*>(sh.red);
+  __syncthreads();                                  // all cst reads done
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int m = incl - nonempty;
+  for (int w = 0; w < warp; ++w) m += wsum[w];
+  uint16_t* cptr = reinterpret_cast<uint16_t*>(sp.cst);
+  uint16_t* ccol = cptr + (kSparseCols + 2);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int d = t * 8 + k;
+    if (d < W && st[k + 1] > st[k]) { cptr[m] = uint16_t(st[k]); ccol[m] = uint16_t(d); ++m; }
+    else if (d < W) wrow[ulo + d] = 0.0;            // empty column: phase A never writes it
+  }
+  if (t == NT - 1) s_nzc = m;                       // last thread holds the total
+  __syncthreads();
+  if (t == 0) cptr[s_nzc] = uint16_t(E);
+  __syncthreads();
+}
+
+// Phase A (sparse): w_j = sum over own rows of P_ij x_i.  The CSC entries are
+// split evenly over the threads (a few columns hold most entries of a CTA, so
+// a thread per column would serialize on them); each thread sums its entries
+// column by column (rows ascending); a column cut by thread boundaries is the
+// left-to-right sum of its pieces, finished by the thread holding its start.
+// Deterministic: the split depends only on the entry count.
+__device__ void phase_a_sparse(const double* x, int64_t r0, int64_t r1, double* wrow, Smem& sh) {
+  const SparseView sp = sparse_view();
+  const int t = threadIdx.x, rows = int(r1 - r0);
+  const uint16_t* cptr = reinterpret_cast<const uint16_t*>(sp.cst);
+  const uint16_t* ccol = cptr + (kSparseCols + 2);
+  double* head = &sh.bp[0][0];                      // per-thread piece of a column begun earlier
+  __syncthreads();
+  for (int r = t; r < rows; r += NT) sp.xs[r] = x[r0 + r];
+  const int ulo = s_win_lo[0], nzc = s_nzc;
+  const int E = cptr[nzc];
+  head[t] = 0.0;
+  __syncthreads();
+  const int kb = int((int64_t(t) * E) / NT), ke = int((int64_t(t + 1) * E) / NT);
+  double tail = 0.0;
+  int tail_m = -1;
+  if (kb < ke) {
+    int lo = 0, hi = nzc;                           // column m of entry kb: cptr[m] <= kb < cptr[m+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (cptr[mid] <= kb) lo = mid; else hi = mid;
+    }
+    int m = lo, mend = cptr[m + 1];
+    bool begun = cptr[m] < kb;                      // column started in an earlier thread
+    double acc = 0.0;
+    int k = kb;
+    while (true) {
+      const int stop = mend < ke ? mend : ke;
+      for (; k + 4 <= stop; k += 4) {
+        int e[4];
+        double pv[4], xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) e[u] = sp.perm[k + u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { pv[u] = sp.val[e[u]]; xv[u] = sp.xs[sp.row[e[u]]]; }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc = fma(pv[u], xv[u], acc);
+      }
+      for (; k < stop; ++k) {
+        const int e = sp.perm[k];
+        acc = fma(sp.val[e], sp.xs[sp.row[e]], acc);
+      }
+      if (begun) head[t] = acc;                     // piece of a column begun earlier
+      else if (mend <= ke) wrow[ulo + ccol[m]] = acc;   // whole column inside this thread
+      else { tail = acc; tail_m = m; }              // column continues in later threads
+      if (mend >= ke) break;
+      ++m;
+      mend = cptr[m + 1];
+      begun = false;
+      acc = 0.0;
+    }
+  }
+  __syncthreads();
+  if (tail_m >= 0) {
+    const int cend = cptr[tail_m + 1];
+    double s = tail;
+    for (int u = t + 1; u < NT && int((int64_t(u) * E) / NT) < cend; ++u) s += head[u];
+    wrow[ulo + ccol[tail_m]] = s;
+  }
+}
+
+// Phase B (sparse): s_i = sum_j P_ij w_j.  The CTA's window of w is staged in
+// shared memory first (one coalesced read); then warp per row, lanes strided
+// over the row's entries, a fixed-tree warp sum.
+__device__ void phase_b_sparse(const double* w, int64_t r0, int64_t r1, double* sv) {
+  const SparseView sp = sparse_view();
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, rows = int(r1 - r0);
+  const int ulo = s_win_lo[0], W = s_win_hi[0] - ulo;
+  double* ws = sp.xs - ulo;                         // ws[j] for window columns j
+  __syncthreads();
+  for (int d = t; d < W; d += NT) sp.xs[d] = __ldcg(w + ulo + d);
+  __syncthreads();
+  for (int r = warp; r < rows; r += NW) {
+    double dot = 0.0;
+    const int e1 = sp.rp[r + 1];
+    int e = sp.rp[r] + lane;
+    for (; e + 96 < e1; e += 128) {
+      double pv[4], wv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { pv[u] = sp.val[e + 32 * u]; wv[u] = ws[sp.col[e + 32 * u]]; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dot = fma(pv[u], wv[u], dot);
+    }
+    for (; e < e1; e += 32) dot = fma(sp.val[e], ws[sp.col[e]], dot);
+    dot = warp_sum(dot);
+    if (lane == 0) sv[r0 + r] = dot;
+  }
+  __syncthreads();
+}
+
 // Phase A: column partials of P^T x over this CTA's rows (ascending).
 __device__ __noinline__ void phase_a(const PlanView v, const double* x, int64_t r0, int64_t r1,
                                      double* wrow, Smem& sh) {
+  if (v.mode == kPlanSparse) {
+    phase_a_sparse(x, r0, r1, wrow, sh);
+    return;
+  }
   const int t = threadIdx.x;
-  const uint32_t ring0 = smem_u32(s_ring) + 16u * t;
-  constexpr uint32_t kSlotBytes = CH * NT * 16;
   const int rows = int(r1 - r0);
   for (int ti = 0; ti < v.nt; ++ti) {
     const int64_t T = int64_t(ti) * TILE;
     const int ulo = s_win_lo[ti], W = s_win_hi[ti] - ulo;
     if (W <= 0) continue;
     const int col0 = ulo + 2 * t;
+    const int nch = (W + 2 * NT - 1) / (2 * NT);
     double2 acc[CH];
 #pragma unroll
     for (int c = 0; c < CH; ++c) acc[c] = make_double2(0.0, 0.0);
@@ -234,34 +606,16 @@ __device__ __noinline__ void phase_a(const PlanView v, const double* x, int64_t 
       __syncthreads();
       for (int k = t; k < m; k += NT) sh.xs[k] = x[r0 + c0 + k];
       __syncthreads();
-      const double* fill_row = v.P + (r0 + c0) * v.ld + T;   // next row to stream
-#pragma unroll
-      for (int d = 0; d < kRingDepth - 1; ++d) {
-        if (d < m) ring_fill(v, fill_row, c0 + d, ti, col0, ring0 + d * kSlotBytes);
-        else cp_commit();
-        fill_row += v.ld;
-      }
-      int slot = 0;
-      uint32_t fdst = ring0 + (kRingDepth - 1) * kSlotBytes;
-      for (int q = 0; q < m; ++q) {
-        if (q + kRingDepth - 1 < m) ring_fill(v, fill_row, c0 + q + kRingDepth - 1, ti, col0, fdst);
-        else cp_commit();
-        fill_row += v.ld;
-        fdst = fdst == ring0 + (kRingDepth - 1) * kSlotBytes ? ring0 : fdst + kSlotBytes;
-        cp_wait<kRingDepth - 1>();
-        int lo, hi;
-        get_span(v, c0 + q, ti, lo, hi);
-        const double xi = sh.xs[q];
-        const double2* row = s_ring + slot * CH * NT + t;
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          if (in_span(col0 + c * NT * 2, lo, hi)) {
-            const double2 pv = row[c * NT];
-            acc[c].x = fma(pv.x, xi, acc[c].x);
-            acc[c].y = fma(pv.y, xi, acc[c].y);
-          }
+      const double* row0 = v.P + (r0 + c0) * v.ld + T;
+      if (v.mode == kPlanRing) {
+        phase_a_ring(v, row0, c0, m, ti, col0, acc, sh);
+      } else {
+        switch (nch) {
+          case 1: phase_a_tile<1>(v, row0, c0, m, ti, col0, acc, sh); break;
+          case 2: phase_a_tile<2>(v, row0, c0, m, ti, col0, acc, sh); break;
+          case 3: phase_a_tile<3>(v, row0, c0, m, ti, col0, acc, sh); break;
+          default: phase_a_tile<4>(v, row0, c0, m, ti, col0, acc, sh); break;
         }
-        slot = slot + 1 == kRingDepth ? 0 : slot + 1;
       }
     }
 #pragma unroll
@@ -333,17 +687,105 @@ __device__ __forceinline__ double warp_reduce8(const double (&d)[8], int lane) {
   return s;
 }
 
+// Phase B over one tile for CTA rows e-1, e-2, ..., e-m (descending), in
+// batches of 8 rows: per-lane dots of the batch, one transpose-reduction, the
+// per-warp partials accumulate in sh.bp[warp][row - c0].
+template <int NCH>
+__device__ __forceinline__ void phase_b_tile(const PlanView& v, const double* row_top, int e,
+                                             int m, int c0, int ti, int col0,
+                                             const double2 (&wv)[CH], Smem& sh) {
+  constexpr int UB = NCH <= 2 ? 8 : 4;               // rows loaded at once
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row_of_lane = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  for (int q0 = 0; q0 < m; q0 += 8) {
+    double d8[8];
+#pragma unroll
+    for (int h = 0; h < 8; h += UB) {
+      double2 pv[UB][NCH];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int q = q0 + h + u;
+        int lo = 0, hi = 0;
+        if (q < m) get_span(v, e - 1 - q, ti, lo, hi);
+        load_row<NCH>(row_top - int64_t(q) * v.ld, lo, hi, col0, pv[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        double dot = 0.0;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          dot = fma(pv[u][c].x, wv[c].x, dot);
+          dot = fma(pv[u][c].y, wv[c].y, dot);
+        }
+        d8[h + u] = dot;
+      }
+    }
+    const double s = warp_reduce8(d8, lane);
+    if ((lane & 3) == 0 && q0 + row_of_lane < m) sh.bp[warp][e - 1 - (q0 + row_of_lane) - c0] += s;
+  }
+}
+
+// Phase B over one wide tile through the ring (same sums as phase_b_tile).
+__device__ __forceinline__ void phase_b_ring(const PlanView& v, const double* fill_row, int e,
+                                             int m, int c0, int ti, int col0,
+                                             const double2 (&wv)[CH], Smem& sh) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int row_of_lane = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  const uint32_t ring0 = smem_u32(s_ring) + 16u * t;
+#pragma unroll
+  for (int d = 0; d < kRingDepth - 1; ++d) {
+    if (d < m) ring_fill(v, fill_row, e - 1 - d, ti, col0, ring0 + d * kSlotBytes);
+    else cp_commit();
+    fill_row -= v.ld;
+  }
+  int slot = 0;
+  uint32_t fdst = ring0 + (kRingDepth - 1) * kSlotBytes;
+  double d8[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) d8[k] = 0.0;
+  for (int q = 0; q < m; ++q) {
+    if (q + kRingDepth - 1 < m) ring_fill(v, fill_row, e - kRingDepth - q, ti, col0, fdst);
+    else cp_commit();
+    fill_row -= v.ld;
+    fdst = fdst == ring0 + (kRingDepth - 1) * kSlotBytes ? ring0 : fdst + kSlotBytes;
+    cp_wait<kRingDepth - 1>();
+    int lo, hi;
+    get_span(v, e - 1 - q, ti, lo, hi);
+    const double2* row = s_ring + slot * CH * NT + t;
+    double dot = 0.0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (in_span(col0 + c * NT * 2, lo, hi)) {
+        const double2 pv = row[c * NT];
+        dot = fma(pv.x, wv[c].x, dot);
+        dot = fma(pv.y, wv[c].y, dot);
+      }
+    }
+    const int b = q & 7;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k == b) d8[k] = dot;
+    if (b == 7 || q == m - 1) {
+      const double s = warp_reduce8(d8, lane);
+      if ((lane & 3) == 0 && row_of_lane <= b) sh.bp[warp][e - 1 - (q - b + row_of_lane) - c0] += s;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) d8[k] = 0.0;
+    }
+    slot = slot + 1 == kRingDepth ? 0 : slot + 1;
+  }
+}
+
 // Phase B: s_i = sum_j P_ij w_j for own rows (DESCENDING: the rows phase A
-// streamed last are the likeliest L2 hits), into sv[i].  Per-lane dots of 8
-// rows are combined by one transpose-reduction; per-warp partials accumulate in
-// shared memory; one fixed-order sum over warps per chunk.
+// streamed last are the likeliest L2 hits), into sv[i].  Per-warp partials
+// accumulate in shared memory; one fixed-order sum over warps per chunk.
 __device__ __noinline__ void phase_b(const PlanView v, const double* w, int64_t r0, int64_t r1,
                                      double* sv, Smem& sh) {
+  if (v.mode == kPlanSparse) {
+    phase_b_sparse(w, r0, r1, sv);
+    return;
+  }
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const uint32_t ring0 = smem_u32(s_ring) + 16u * t;
-  constexpr uint32_t kSlotBytes = CH * NT * 16;
   const int rows = int(r1 - r0);
-  const int row_of_lane = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
   for (int e = rows; e > 0; e -= kRows) {          // chunk [e - m, e) of CTA rows
     const int m = min(e, kRows), c0 = e - m;
     for (int k = lane; k < m; k += 32) sh.bp[warp][k] = 0.0;
@@ -353,53 +795,23 @@ __device__ __noinline__ void phase_b(const PlanView v, const double* w, int64_t 
       const int ulo = s_win_lo[ti], W = s_win_hi[ti] - ulo;
       if (W <= 0) continue;
       const int col0 = ulo + 2 * t;
+      const int nch = (W + 2 * NT - 1) / (2 * NT);
       double2 wv[CH];
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         const int rel = c * NT * 2 + 2 * t;
         wv[c] = rel < W ? ldcg2(w + T + ulo + rel) : make_double2(0.0, 0.0);
       }
-      const double* fill_row = v.P + (r0 + e - 1) * v.ld + T;
-#pragma unroll
-      for (int d = 0; d < kRingDepth - 1; ++d) {
-        if (d < m) ring_fill(v, fill_row, e - 1 - d, ti, col0, ring0 + d * kSlotBytes);
-        else cp_commit();
-        fill_row -= v.ld;
-      }
-      int slot = 0;
-      uint32_t fdst = ring0 + (kRingDepth - 1) * kSlotBytes;
-      double d8[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) d8[k] = 0.0;
-      for (int q = 0; q < m; ++q) {
-        if (q + kRingDepth - 1 < m) ring_fill(v, fill_row, e - kRingDepth - q, ti, col0, fdst);
-        else cp_commit();
-        fill_row -= v.ld;
-        fdst = fdst == ring0 + (kRingDepth - 1) * kSlotBytes ? ring0 : fdst + kSlotBytes;
-        cp_wait<kRingDepth - 1>();
-        int lo, hi;
-        get_span(v, e - 1 - q, ti, lo, hi);
-        const double2* row = s_ring + slot * CH * NT + t;
-        double dot = 0.0;
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          if (in_span(col0 + c * NT * 2, lo, hi)) {
-            const double2 pv = row[c * NT];
-            dot = fma(pv.x, wv[c].x, dot);
-            dot = fma(pv.y, wv[c].y, dot);
-          }
+      const double* row_top = v.P + (r0 + e - 1) * v.ld + T;
+      if (v.mode == kPlanRing) {
+        phase_b_ring(v, row_top, e, m, c0, ti, col0, wv, sh);
+      } else {
+        switch (nch) {
+          case 1: phase_b_tile<1>(v, row_top, e, m, c0, ti, col0, wv, sh); break;
+          case 2: phase_b_tile<2>(v, row_top, e, m, c0, ti, col0, wv, sh); break;
+          case 3: phase_b_tile<3>(v, row_top, e, m, c0, ti, col0, wv, sh); break;
+          default: phase_b_tile<4>(v, row_top, e, m, c0, ti, col0, wv, sh); break;
         }
-        const int b = q & 7;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (k == b) d8[k] = dot;
-        if (b == 7 || q == m - 1) {
-          const double s = warp_reduce8(d8, lane);
-          if ((lane & 3) == 0 && row_of_lane <= b) sh.bp[warp][e - 1 - (q - b + row_of_lane) - c0] += s;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) d8[k] = 0.0;
-        }
-        slot = slot + 1 == kRingDepth ? 0 : slot + 1;
       }
     }
     __syncthreads();
@@ -514,13 +926,16 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
   __shared__ Smem sh;
   cg::grid_group grid = cg::this_grid();
   const int G = gridDim.x;
-  const int64_t r0 = (int64_t(blockIdx.x) * a.n) / G;
-  const int64_t r1 = (int64_t(blockIdx.x + 1) * a.n) / G;
+  const int64_t r0 = a.part[blockIdx.x];             // rows [r0, r1): k_partition
+  const int64_t r1 = a.part[blockIdx.x + 1];
+  if (threadIdx.x == 0) s_mode = a.part[G + 1];
   int slot = 0;
   int64_t nh = 0;
   DevResult res{};
   res.status = OTN_OK;
+  __syncthreads();
   stage_layout(a, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld);
+  if (s_mode == kPlanSparse) stage_sparse(a, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
 
   if (a.pre_flags) {
     // [0]: plan overflow (materialize), [1]: nonpositive sums (system prep);
@@ -644,22 +1059,145 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.res = res;
 }
 
-constexpr size_t kRingBytes = size_t(kRingDepth) * CH * NT * sizeof(double2);
+constexpr size_t kRingBytes = size_t(kRingDepth) * kSlotBytes;
+constexpr size_t kDynBytes = kRingBytes > kSparseBytes ? kRingBytes : kSparseBytes;
+
+// ---------------------------------------------------------------------------
+// k_partition: one CTA picks the plan mode of the next k_coop launch and its
+// row partition (integer arithmetic only: deterministic).
+//   part[0..G] = row boundaries of the G CTAs, part[G+1] = PlanMode.
+// Sparse (one tile, ld <= 4096): rows balanced on cost_i = nnz_i + 32, row i
+// going to CTA floor(prefix_i * G / total); used if every CTA's rows and
+// nonzeros fit its shared memory.  Otherwise equal rows (the streaming phases
+// cost ~ rows x window chunks; a span-balanced split measured slower), and
+// kPlanL2 when the sum of the row spans fits the L2 budget.
+// ---------------------------------------------------------------------------
+constexpr int kPartThreads = 1024;
+constexpr int kPartRows = kSparseCols;               // rows handled in shared memory
+
+__device__ __forceinline__ int64_t row_span(const uint64_t* mask, int64_t ld, int64_t mw,
+                                            int64_t i) {
+  int64_t span = 0;
+  const int nt = ntiles_of(ld);
+  for (int ti = 0; ti < nt; ++ti) {
+    const uint64_t bits = __ldg(mask + i * mw + ti);
+    if (!bits) continue;
+    const int64_t T = int64_t(ti) * TILE;
+    const int64_t width = ld - T < TILE ? ld - T : int64_t(TILE);
+    const int64_t lo = int64_t(__ffsll(static_cast<long long>(bits)) - 1) * kSegCols;
+    int64_t hi = int64_t(64 - __clzll(static_cast<long long>(bits))) * kSegCols;
+    if (hi > width) hi = width;
+    span += hi - lo;
+  }
+  return span;
+}
+
+template <typename T>
+__device__ T block_sum_part(T v, T* buf) {                // all threads get the total
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) buf[warp] = v;
+  __syncthreads();
+  T tot = 0;
+  for (int w = 0; w < kPartThreads / 32; ++w) tot += buf[w];
+  return tot;
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_partition(const uint64_t* mask, int64_t n,
+                                                            int64_t ld, int64_t mw, int G,
+                                                            int* part) {
+  __shared__ int s_pref[kPartRows + 1];      // inclusive prefix of the sparse row costs
+  __shared__ int64_t s_buf[32];
+  __shared__ int s_ibuf[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int mode = n * ld * 8 <= kL2ModeBytes ? kPlanL2 : kPlanRing;
+  bool sparse = false;
+  if (mask) {
+    int64_t sp = 0, nz = 0;
+    for (int64_t i = t; i < n; i += kPartThreads) {
+      sp += row_span(mask, ld, mw, i);
+      nz += int64_t(__ldg(mask + i * mw + mw - 1));
+    }
+    sp = block_sum_part<int64_t>(sp, s_buf);
+    nz = block_sum_part<int64_t>(nz, s_buf);
+    mode = sp * 8 <= kL2ModeBytes ? kPlanL2 : kPlanRing;
+    sparse = ld <= kSparseCols && n <= kPartRows && nz * 5 <= int64_t(G) * kSparseCap * 4;
+  }
+  if (sparse) {
+    // inclusive prefix of cost_i over rows: 4 contiguous rows per thread
+    constexpr int R = kPartRows / kPartThreads;
+    int c[R], run = 0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int64_t i = int64_t(t) * R + k;
+      c[k] = i < n ? int(__ldg(mask + i * mw + mw - 1)) + 32 : 0;
+      run += c[k];
+    }
+    int incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) s_ibuf[warp] = incl;
+    __syncthreads();
+    int off = incl - run;
+    for (int w = 0; w < warp; ++w) off += s_ibuf[w];
+    if (t == 0) s_pref[0] = 0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      off += c[k];
+      const int64_t i = int64_t(t) * R + k;
+      if (i < n) s_pref[i + 1] = off;
+    }
+    __syncthreads();
+    const int64_t total = s_pref[n] > 0 ? s_pref[n] : 1;
+    // CTA of row i: floor(pref_excl(i) * G / total); part[b] = first row of CTA >= b
+    for (int64_t i = t; i < n; i += kPartThreads) {
+      const int cb = int(int64_t(s_pref[i]) * G / total);
+      const int pb = i == 0 ? -1 : int(int64_t(s_pref[i - 1]) * G / total);
+      for (int k = pb + 1; k <= cb; ++k) part[k] = int(i);
+    }
+    const int last = int(int64_t(s_pref[n - 1]) * G / total);
+    for (int k = last + 1 + t; k <= G; k += kPartThreads) part[k] = int(n);
+    __syncthreads();
+    int bad = 0;
+    for (int b = t; b < G; b += kPartThreads) {
+      const int r0 = part[b], r1 = part[b + 1];
+      const int rows = r1 - r0, nnz = s_pref[r1] - s_pref[r0] - 32 * rows;
+      if (rows > kSparseRows || nnz > kSparseCap) bad = 1;
+    }
+    sparse = block_sum_part<int>(bad, s_ibuf) == 0;
+  }
+  __syncthreads();
+  if (sparse) {
+    if (t == 0) part[G + 1] = kPlanSparse;
+    return;
+  }
+  for (int b = t; b <= G; b += kPartThreads) part[b] = int((int64_t(b) * n) / G);
+  if (t == 0) part[G + 1] = mode;
+}
 
 cudaError_t launch_coop(otn_ctx* x, const CoopArgs& a0) {
   CoopArgs a = a0;
   a.stages = kRingDepth;
+  a.part = x->part;
+  k_partition<<<1, kPartThreads, 0, x->stream>>>(a.mask, a.n, a.ld, a.mw, x->coop_blocks, x->part);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
   void* args[] = {&a};
   return cudaLaunchCooperativeKernel((void*)k_coop, dim3(x->coop_blocks), dim3(NT), args,
-                                     kRingBytes, x->stream);
+                                     kDynBytes, x->stream);
 }
 
 int coop_occupancy(int* blocks_per_sm) {
   cudaError_t e = cudaFuncSetAttribute(k_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(kRingBytes));
+                                       int(kDynBytes));
   if (e != cudaSuccess) return int(e);
   return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_coop, NT,
-                                                            kRingBytes);
+                                                            kDynBytes);
 }
 
 }  // namespace otn

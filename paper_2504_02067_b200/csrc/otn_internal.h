@@ -47,6 +47,7 @@ struct otn_ctx {
   double* lse_part;       // lse_slabs x ld x 2 (m, s) column-LSE partials
   double* scal;           // 64 device scalars
   int* flags;             // 16 device flag words
+  int* part;              // coop_blocks + 2 ints: row partition + plan mode (k_partition)
   otn::DevResult* dres;
   // pinned host mirrors
   double* h_scal;
@@ -92,6 +93,7 @@ struct CoopArgs {
   int64_t mw;
   int stages;             // shared-memory ring stages (set by launch_coop)
   int pad2;
+  const int* part;        // row partition + plan mode (k_partition, set by launch_coop)
   // workspace
   double *r, *z, *p, *q, *M, *wc, *sv, *wpart, *red;
   DevResult* res;

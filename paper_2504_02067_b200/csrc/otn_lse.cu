@@ -166,9 +166,10 @@ __global__ void __launch_bounds__(kLseThreads) k_materialize(const double* __res
   const double* crow = C + row * ld;
   double* prow = P + row * ld;
   const double ui = __ldg(u + row);
-  const int64_t mw = (ld + kSegWordCols - 1) / kSegWordCols;
+  const int64_t mw = OTN_MASK_WORDS(ld);
   double acc = 0.0, mx = OTN_NINF;
   uint64_t bits = 0;
+  int nnz = 0;
   for (int64_t base = 0; base < ld; base += 256) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(kLseThreads) k_materialize(const double* __res
         const double p0 = exp_fast(e0), p1 = exp_fast(e1);
         *reinterpret_cast<double2*>(prow + j) = make_double2(p0, p1);
         nz = (p0 != 0.0) || (p1 != 0.0);
+        nnz += int(p0 != 0.0) + int(p1 != 0.0);
         if (icP) {
           if (j < n) acc = fma(__dmul_rn(p0, p0), __ldg(icP + j), acc);
           if (j + 1 < n) acc = fma(__dmul_rn(p1, p1), __ldg(icP + j + 1), acc);
@@ -200,6 +202,10 @@ __global__ void __launch_bounds__(kLseThreads) k_materialize(const double* __res
   }
   mx = warp_max(mx);
   if (icP) acc = warp_sum(acc);
+  if (mask) {
+    nnz = warp_sum_int(nnz);
+    if (lane == 0) mask[row * mw + mw - 1] = uint64_t(nnz);   // count word
+  }
   if (lane == 0) {
     if (mx > 700.0) atomicOr(flag, 1);          // _kernels.py:53-58
     if (icP) mu[row] = __ddiv_rn(acc, __ldg(rP + row));
@@ -213,14 +219,16 @@ __global__ void __launch_bounds__(kLseThreads) k_plan_mask(const double* __restr
   const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
-  const int64_t mw = (ld + kSegWordCols - 1) / kSegWordCols;
+  const int64_t mw = OTN_MASK_WORDS(ld);
   uint64_t bits = 0;
+  int nnz = 0;
   for (int64_t base = 0; base < ld; base += 64) {
     const int64_t j = base + 2 * lane;
     bool nz = false;
     if (j < ld) {
       const double2 p = ld_stream2(P + row * ld + j);
       nz = (p.x != 0.0) || (p.y != 0.0);
+      nnz += int(p.x != 0.0) + int(p.y != 0.0);
     }
     if (__ballot_sync(0xffffffffu, nz)) bits |= 1ull << ((base >> 6) & 63);
     if (((base + 64) % kSegWordCols) == 0 || base + 64 >= ld) {
@@ -228,6 +236,8 @@ __global__ void __launch_bounds__(kLseThreads) k_plan_mask(const double* __restr
       bits = 0;
     }
   }
+  nnz = warp_sum_int(nnz);
+  if (lane == 0) mask[row * mw + mw - 1] = uint64_t(nnz);   // count word
 }
 
 __global__ void k_sys_prep(int64_t n, const double* __restrict__ lr, const double* __restrict__ lc,

@@ -212,3 +212,55 @@ def test_exp_fast_accuracy():
     # ulp distance on the IEEE bit patterns (monotone for non-negative doubles)
     ulps = np.abs(g.view(np.int64) - w.view(np.int64))
     assert ulps.max() <= 1, (ulps.max(), x[ok][np.argmax(ulps)])
+
+
+def _layout(sysd):
+    k = sysd._ctx
+    G = k.coop_blocks
+    lay = np.zeros(G + 2, dtype=np.int32)
+    k.call("otn_coop_layout", lay.ctypes.data)
+    return lay[: G + 1], int(lay[G + 1])
+
+
+def _sparse_plan(n, per_row, seed, heavy=0):
+    """Banded-random sparse plan with exact zeros elsewhere (+ a few heavy rows)."""
+    rng = np.random.default_rng(seed)
+    P = np.zeros((n, n))
+    for i in range(n):
+        k = per_row if i >= heavy else min(n, 40 * per_row)
+        cols = np.unique((i + rng.integers(-3 * per_row, 3 * per_row + 1, size=k)) % n)
+        P[i, cols] = rng.random(len(cols)) * 10.0 ** rng.uniform(-300, 0, len(cols))
+    P[np.arange(n), np.arange(n)] += 1.0           # positive row / column sums
+    return P
+
+
+@pytest.mark.parametrize("n,per_row,heavy,mode", [
+    (64, 3, 0, 2), (300, 8, 0, 2), (1024, 20, 5, 2), (4096, 12, 9, 2),
+    (1024, 1024, 0, 2), (2048, 2048, 0, 1), (4096, 4096, 0, 0)])
+def test_hvp_plan_modes(n, per_row, heavy, mode):
+    """Every plan mode (0 streamed ring, 1 L2-direct, 2 sparse shared-memory rows)
+    against numpy on the same plan; the sparse mode also on heavy rows."""
+    if per_row >= n:
+        rng = np.random.default_rng(n)
+        P = rng.random((n, n)) + 0.01
+    else:
+        P = _sparse_plan(n, per_row, seed=n + heavy, heavy=heavy)
+    rP, cP = P.sum(1), P.sum(0)
+    sysd = DiscountedSystem(P, rP, cP)
+    d = np.random.default_rng(7).standard_normal(n)
+    got_pc = sysd.apply_pc(d)
+    part, got_mode = _layout(sysd)
+    assert got_mode == mode
+    assert part[0] == 0 and part[-1] == n and np.all(np.diff(part) >= 0)
+    want_pc = (P.T @ d) / cP
+    np.testing.assert_allclose(got_pc, want_pc, rtol=1e-12, atol=1e-14 * np.abs(want_pc).max())
+    for rho in (0.5, 1.0):
+        want = rP * d - rho * (P @ ((P.T @ d) / cP))
+        np.testing.assert_allclose(sysd.apply_F(rho, d), want, rtol=1e-11,
+                                   atol=1e-13 * np.abs(want).max())
+    want_prc = (P @ ((P.T @ d) / cP)) / rP
+    np.testing.assert_allclose(sysd.apply_prc(d), want_prc, rtol=1e-12,
+                               atol=1e-14 * np.abs(want_prc).max())
+    x, _ = pcg_solve(sysd, 0.9, -d, 1e-10 * np.abs(d).sum())
+    F = np.diag(rP) - 0.9 * (P / cP) @ P.T
+    np.testing.assert_allclose(F @ x, -d, rtol=1e-6, atol=1e-9 * np.abs(d).max())
