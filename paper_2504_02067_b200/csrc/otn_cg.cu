@@ -39,7 +39,8 @@ struct Smem {
   double red[4][33];
   double gres[4];
   double a2[NW][33];
-  double xs[kRows];                 // phase A: this chunk's x_i
+  double xs[NT];                    // phase A input: x of the CTA's rows (row - r0)
+  double sv[NT];                    // phase B output: (P w) of the CTA's rows
   double bp[NW][kRows];             // phase B: per-warp partial row dots
 };
 
@@ -111,7 +112,6 @@ __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&v)[K]
 // ---------------------------------------------------------------------------
 constexpr int kSpanSmem = 8192;                     // (row, tile) spans staged per CTA (32 KB)
 constexpr int kMaxTiles = 64;                       // ld <= 262144
-__shared__ uint32_t s_span[kSpanSmem];              // lo | hi << 16, relative to the tile
 __shared__ int s_win_lo[kMaxTiles], s_win_hi[kMaxTiles];
 // Plan mode of this launch (chosen by k_partition, uniform over the grid):
 //   kPlanRing    plan streamed from HBM through per-thread cp.async rings;
@@ -122,6 +122,9 @@ __shared__ int s_win_lo[kMaxTiles], s_win_hi[kMaxTiles];
 enum PlanMode { kPlanRing = 0, kPlanL2 = 1, kPlanSparse = 2 };
 __shared__ int s_mode;
 __shared__ int s_nzc;                               // kPlanSparse: nonempty columns of the CTA
+__shared__ int s_split;                             // kPlanSparse: threads splitting the CSC entries
+__shared__ uint16_t s_m0[kCoopThreads];             // kPlanSparse: column of each thread's first entry
+__shared__ int s_kb[kCoopThreads + 1];              // kPlanSparse: first CSC entry of each thread
 constexpr int64_t kL2ModeBytes = 80ll * 1024 * 1024;
 
 // Everything the streaming loops need, by value (registers, not the kernel's
@@ -132,6 +135,7 @@ struct PlanView {
   int64_t ld, mw;
   int nt;                   // tiles
   int mode;                 // PlanMode
+  uint32_t* span;           // staged spans: lo | hi << 16, relative to the tile
 };
 
 // Plans too large for L2 (kPlanRing: streamed from HBM) use a per-thread
@@ -139,7 +143,28 @@ struct PlanView {
 // continuously (the register batches drain between batches, which costs HBM
 // bandwidth; on L2-resident spans the ring is the slower one).
 constexpr int kRingDepth = 5;
-extern __shared__ __align__(128) double2 s_ring[];  // [kRingDepth][CH][NT] double2
+extern __shared__ __align__(128) double2 s_ring[];  // dynamic: ring or sparse rows, then spans
+constexpr size_t kRingBytes = size_t(kRingDepth) * CH * NT * 16;
+
+// kPlanSparse shared-memory layout (dynamic region; see the sparse section).
+constexpr int kSparseRows = 512;                    // rows per CTA
+constexpr int kSparseCols = TILE;                   // one tile (ld <= 4096)
+constexpr int kSparseCap = 10900;                   // nonzeros per CTA (fits 227 KB with the statics)
+constexpr size_t kSparseXs = 0;                     // double[kSparseCols]: x rows (A) / w window (B)
+constexpr size_t kSparseRp = kSparseXs + kSparseCols * 8;               // int[kSparseRows + 1]
+constexpr size_t kSparseCst = kSparseRp + (kSparseRows + 4) * 4;        // int[kSparseCols + 1]
+constexpr size_t kSparseVal = kSparseCst + (kSparseCols + 4) * 4;       // double[cap]
+constexpr size_t kSparseCol = kSparseVal + size_t(kSparseCap) * 8;      // u16[cap]
+constexpr size_t kSparseRow = kSparseCol + size_t(kSparseCap) * 2;      // u16[cap]
+constexpr size_t kSparsePerm = kSparseRow + size_t(kSparseCap) * 2;     // u16[cap]
+constexpr size_t kSparseBytes = kSparsePerm + size_t(kSparseCap) * 2;
+
+// The (row, tile) spans live in the dynamic region after what the mode uses.
+__device__ __forceinline__ uint32_t* span_base(int mode) {
+  char* b = reinterpret_cast<char*>(s_ring);
+  return reinterpret_cast<uint32_t*>(b + (mode == kPlanRing ? kRingBytes
+                                          : mode == kPlanSparse ? kSparseBytes : 0));
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -168,7 +193,7 @@ __device__ __forceinline__ void mask_span(const PlanView& v, int64_t i, int ti, 
 
 // Span of row r0 + il (il = row index within the CTA) in tile ti.
 __device__ __forceinline__ void get_span(const PlanView& v, int il, int ti, int& lo, int& hi) {
-  const uint32_t s = s_span[il * v.nt + ti];
+  const uint32_t s = v.span[il * v.nt + ti];
   lo = int(s & 0xffffu);
   hi = int(s >> 16);
 }
@@ -187,6 +212,7 @@ __device__ PlanView plan_view(const CoopArgs& a, int64_t r0, int64_t r1) {
   v.mw = a.mw;
   v.nt = ntiles_of(a.ld);
   v.mode = s_mode;
+  v.span = span_base(v.mode);
   return v;
 }
 
@@ -202,7 +228,7 @@ __device__ void stage_layout(const CoopArgs& a, int64_t r0, int64_t r1, double* 
     const int ti = int(k % v.nt);
     int lo, hi;
     mask_span(v, r0 + k / v.nt, ti, lo, hi);
-    s_span[k] = uint32_t(lo) | (uint32_t(hi) << 16);
+    v.span[k] = uint32_t(lo) | (uint32_t(hi) << 16);
     if (lo < hi) {
       atomicMin(&s_win_lo[ti], lo);
       atomicMax(&s_win_hi[ti], hi);
@@ -243,7 +269,7 @@ __device__ __forceinline__ void phase_a_tile(const PlanView& v, const double* ro
     for (int u = 0; u < U; ++u) {
       int lo = 0, hi = 0;
       if (q0 + u < m) get_span(v, c0 + q0 + u, ti, lo, hi);
-      xi[u] = sh.xs[q0 + u < m ? q0 + u : 0];
+      xi[u] = sh.xs[c0 + (q0 + u < m ? q0 + u : 0)];
       load_row<NCH>(row0 + int64_t(q0 + u) * v.ld, lo, hi, col0, pv[u]);
     }
 #pragma unroll
@@ -294,7 +320,7 @@ __device__ __forceinline__ void phase_a_ring(const PlanView& v, const double* fi
     cp_wait<kRingDepth - 1>();
     int lo, hi;
     get_span(v, c0 + q, ti, lo, hi);
-    const double xi = sh.xs[q];
+    const double xi = sh.xs[c0 + q];
     const double2* row = s_ring + slot * CH * NT + threadIdx.x;
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
@@ -322,17 +348,6 @@ __device__ __forceinline__ void phase_a_ring(const PlanView& v, const double* fi
 // k_partition chooses this mode and a row partition balanced on nonzeros, and
 // guarantees the capacities below.
 // ---------------------------------------------------------------------------
-constexpr int kSparseRows = 512;                    // rows per CTA
-constexpr int kSparseCols = TILE;                   // one tile (ld <= 4096)
-constexpr int kSparseCap = 9200;                    // nonzeros per CTA
-constexpr size_t kSparseXs = 0;                     // double[kSparseCols]: x rows (A) / w window (B)
-constexpr size_t kSparseRp = kSparseXs + kSparseCols * 8;               // int[kSparseRows + 1]
-constexpr size_t kSparseCst = kSparseRp + (kSparseRows + 4) * 4;        // int[kSparseCols + 1]
-constexpr size_t kSparseVal = kSparseCst + (kSparseCols + 4) * 4;       // double[cap]
-constexpr size_t kSparseCol = kSparseVal + size_t(kSparseCap) * 8;      // u16[cap]
-constexpr size_t kSparseRow = kSparseCol + size_t(kSparseCap) * 2;      // u16[cap]
-constexpr size_t kSparsePerm = kSparseRow + size_t(kSparseCap) * 2;     // u16[cap]
-constexpr size_t kSparseBytes = kSparsePerm + size_t(kSparseCap) * 2;
 
 struct SparseView {
   double* xs;
@@ -485,6 +500,22 @@ __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* 
   if (t == NT - 1) s_nzc = m;                       // last thread holds the total
   __syncthreads();
   if (t == 0) cptr[s_nzc] = uint16_t(E);
+  // phase A splits the CSC entries over `split` threads, >= 8 entries each
+  // (fewer, longer pieces: a column cut in many pieces is summed serially)
+  const int split = E / 8 < 1 ? 1 : (E / 8 < NT ? E / 8 : NT);
+  if (t == 0) s_split = split;
+  __syncthreads();
+  s_kb[t] = t < split ? int((int64_t(t) * E) / split) : E;
+  if (t == 0) s_kb[NT] = E;
+  if (t < split) {
+    const int kb = int((int64_t(t) * E) / split);
+    int lo = 0, hi = s_nzc;                         // cptr[lo] <= kb < cptr[lo + 1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (cptr[mid] <= kb) lo = mid; else hi = mid;
+    }
+    s_m0[t] = uint16_t(lo);
+  }
   __syncthreads();
 }
 
@@ -494,27 +525,21 @@ __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* 
 // column by column (rows ascending); a column cut by thread boundaries is the
 // left-to-right sum of its pieces, finished by the thread holding its start.
 // Deterministic: the split depends only on the entry count.
-__device__ void phase_a_sparse(const double* x, int64_t r0, int64_t r1, double* wrow, Smem& sh) {
+__device__ void phase_a_sparse(int64_t r0, int64_t r1, double* wrow, Smem& sh) {
   const SparseView sp = sparse_view();
   const int t = threadIdx.x, rows = int(r1 - r0);
   const uint16_t* cptr = reinterpret_cast<const uint16_t*>(sp.cst);
   const uint16_t* ccol = cptr + (kSparseCols + 2);
   double* head = &sh.bp[0][0];                      // per-thread piece of a column begun earlier
-  __syncthreads();
-  for (int r = t; r < rows; r += NT) sp.xs[r] = x[r0 + r];
-  const int ulo = s_win_lo[0], nzc = s_nzc;
-  const int E = cptr[nzc];
+  const double* xs = sh.xs;
+  const int ulo = s_win_lo[0];
   head[t] = 0.0;
   __syncthreads();
-  const int kb = int((int64_t(t) * E) / NT), ke = int((int64_t(t + 1) * E) / NT);
+  const int kb = s_kb[t], ke = s_kb[t + 1];
   double tail = 0.0;
   int tail_m = -1;
   if (kb < ke) {
-    int lo = 0, hi = nzc;                           // column m of entry kb: cptr[m] <= kb < cptr[m+1]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (cptr[mid] <= kb) lo = mid; else hi = mid;
-    }
+    const int lo = s_m0[t];
     int m = lo, mend = cptr[m + 1];
     bool begun = cptr[m] < kb;                      // column started in an earlier thread
     double acc = 0.0;
@@ -527,13 +552,13 @@ __device__ void phase_a_sparse(const double* x, int64_t r0, int64_t r1, double* 
 #pragma unroll
         for (int u = 0; u < 4; ++u) e[u] = sp.perm[k + u];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) { pv[u] = sp.val[e[u]]; xv[u] = sp.xs[sp.row[e[u]]]; }
+        for (int u = 0; u < 4; ++u) { pv[u] = sp.val[e[u]]; xv[u] = xs[sp.row[e[u]]]; }
 #pragma unroll
         for (int u = 0; u < 4; ++u) acc = fma(pv[u], xv[u], acc);
       }
       for (; k < stop; ++k) {
         const int e = sp.perm[k];
-        acc = fma(sp.val[e], sp.xs[sp.row[e]], acc);
+        acc = fma(sp.val[e], xs[sp.row[e]], acc);
       }
       if (begun) head[t] = acc;                     // piece of a column begun earlier
       else if (mend <= ke) wrow[ulo + ccol[m]] = acc;   // whole column inside this thread
@@ -549,7 +574,7 @@ __device__ void phase_a_sparse(const double* x, int64_t r0, int64_t r1, double* 
   if (tail_m >= 0) {
     const int cend = cptr[tail_m + 1];
     double s = tail;
-    for (int u = t + 1; u < NT && int((int64_t(u) * E) / NT) < cend; ++u) s += head[u];
+    for (int u = t + 1; s_kb[u] < cend; ++u) s += head[u];   // s_kb[split..NT] = E
     wrow[ulo + ccol[tail_m]] = s;
   }
 }
@@ -557,7 +582,7 @@ __device__ void phase_a_sparse(const double* x, int64_t r0, int64_t r1, double* 
 // Phase B (sparse): s_i = sum_j P_ij w_j.  The CTA's window of w is staged in
 // shared memory first (one coalesced read); then warp per row, lanes strided
 // over the row's entries, a fixed-tree warp sum.
-__device__ void phase_b_sparse(const double* w, int64_t r0, int64_t r1, double* sv) {
+__device__ void phase_b_sparse(const double* w, int64_t r0, int64_t r1, double* sv) {   // sv: sh.sv
   const SparseView sp = sparse_view();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, rows = int(r1 - r0);
   const int ulo = s_win_lo[0], W = s_win_hi[0] - ulo;
@@ -578,16 +603,17 @@ __device__ void phase_b_sparse(const double* w, int64_t r0, int64_t r1, double* 
     }
     for (; e < e1; e += 32) dot = fma(sp.val[e], ws[sp.col[e]], dot);
     dot = warp_sum(dot);
-    if (lane == 0) sv[r0 + r] = dot;
+    if (lane == 0) sv[r] = dot;
   }
   __syncthreads();
 }
 
 // Phase A: column partials of P^T x over this CTA's rows (ascending).
-__device__ __noinline__ void phase_a(const PlanView v, const double* x, int64_t r0, int64_t r1,
-                                     double* wrow, Smem& sh) {
+// Input: sh.xs[row - r0] (filled by the caller, followed by a barrier).
+__device__ __noinline__ void phase_a(const PlanView v, int64_t r0, int64_t r1, double* wrow,
+                                     Smem& sh) {
   if (v.mode == kPlanSparse) {
-    phase_a_sparse(x, r0, r1, wrow, sh);
+    phase_a_sparse(r0, r1, wrow, sh);
     return;
   }
   const int t = threadIdx.x;
@@ -603,9 +629,6 @@ __device__ __noinline__ void phase_a(const PlanView v, const double* x, int64_t 
     for (int c = 0; c < CH; ++c) acc[c] = make_double2(0.0, 0.0);
     for (int c0 = 0; c0 < rows; c0 += kRows) {
       const int m = min(rows - c0, kRows);
-      __syncthreads();
-      for (int k = t; k < m; k += NT) sh.xs[k] = x[r0 + c0 + k];
-      __syncthreads();
       const double* row0 = v.P + (r0 + c0) * v.ld + T;
       if (v.mode == kPlanRing) {
         phase_a_ring(v, row0, c0, m, ti, col0, acc, sh);
@@ -778,10 +801,11 @@ __device__ __forceinline__ void phase_b_ring(const PlanView& v, const double* fi
 // Phase B: s_i = sum_j P_ij w_j for own rows (DESCENDING: the rows phase A
 // streamed last are the likeliest L2 hits), into sv[i].  Per-warp partials
 // accumulate in shared memory; one fixed-order sum over warps per chunk.
+// Output: sh.sv[row - r0] (complete after the closing barrier).
 __device__ __noinline__ void phase_b(const PlanView v, const double* w, int64_t r0, int64_t r1,
-                                     double* sv, Smem& sh) {
+                                     Smem& sh) {
   if (v.mode == kPlanSparse) {
-    phase_b_sparse(w, r0, r1, sv);
+    phase_b_sparse(w, r0, r1, sh.sv);
     return;
   }
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -819,30 +843,49 @@ __device__ __noinline__ void phase_b(const PlanView v, const double* w, int64_t 
       double tot = 0.0;
 #pragma unroll
       for (int ww = 0; ww < NW; ++ww) tot += sh.bp[ww][t];
-      sv[r0 + c0 + t] = tot;
+      sh.sv[c0 + t] = tot;
     }
     __syncthreads();
   }
 }
 
-// q = F(rho) x on own rows (newton.py:100-105; matvecs skipped when rho == 0).
-__device__ void hvp(cg::grid_group& grid, const CoopArgs& a, const double* x, double rho,
-                    double* q, int64_t r0, int64_t r1, Smem& sh, int64_t& nh) {
+// ---------------------------------------------------------------------------
+// CG state in registers.  Every CTA owns at most NT rows (k_partition and
+// launch_coop guarantee it), so thread t holds row r0 + t of every CG vector
+// (x, r, z, p, q, the Jacobi diagonal) in registers for the whole launch; only
+// the plan phases exchange data, through sh.xs / sh.sv and the column
+// workspace.  Threads without a row hold zeros (and M = 1): they add nothing
+// to any reduction.
+// ---------------------------------------------------------------------------
+struct Row {
+  bool own;
+  int64_t i;                                        // global row (valid when own)
+};
+
+// A^T x partials of the CTA rows for x held one value per thread.
+__device__ __forceinline__ void stage_x(double xv, Smem& sh) {
+  __syncthreads();                                  // previous readers of sh.xs are done
+  sh.xs[threadIdx.x] = xv;
+  __syncthreads();
+}
+
+// q = F(rho) x for the thread's row (newton.py:100-105; matvecs skipped when
+// rho == 0): q = rP x - rho * P((P^T x) / cP).
+__device__ double hvp(cg::grid_group& grid, const CoopArgs& a, double xv, double rho, double rPi,
+                      int64_t r0, int64_t r1, Smem& sh, int64_t& nh) {
+  double o = __dmul_rn(rPi, xv);
   if (rho != 0.0) {
     ++nh;
-    __syncthreads();
-    phase_a(plan_view(a, r0, r1), x, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
+    stage_x(xv, sh);
+    phase_a(plan_view(a, r0, r1), r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
     grid.sync();
     phase_a2(a, 0, a.wc, sh);
     grid.sync();
-    phase_b(plan_view(a, r0, r1), a.wc, r0, r1, a.sv, sh);
+    phase_b(plan_view(a, r0, r1), a.wc, r0, r1, sh);   // ends with a barrier
+    if (int64_t(threadIdx.x) < r1 - r0) o = __dsub_rn(o, __dmul_rn(rho, sh.sv[threadIdx.x]));
+    else o = 0.0;                                   // no row: sh.sv is not written there
   }
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += NT) {
-    double o = __dmul_rn(__ldg(a.rP + i), x[i]);
-    if (rho != 0.0) o = __dsub_rn(o, __dmul_rn(rho, a.sv[i]));
-    q[i] = o;
-  }
-  __syncthreads();
+  return o;
 }
 
 struct PcgOut {
@@ -851,31 +894,33 @@ struct PcgOut {
   double resid;
 };
 
-// Jacobi-PCG, newton.py:123-172.  b == nullptr means b = -g.
-__device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, double rho, const double* bvec,
-                      double tol, double* x, bool has_x0, int64_t max_iters, int64_t r0,
-                      int64_t r1, int& slot, Smem& sh, int64_t& nh) {
+// Jacobi-PCG, newton.py:123-172, on register rows.  b == nullptr means b = -g.
+// x: in (if has_x0) / out.
+__device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, double rPi,
+                      double rho, const double* bvec, double tol, double& x, bool has_x0,
+                      int64_t max_iters, int64_t r0, int64_t r1, int& slot, Smem& sh,
+                      int64_t& nh) {
   PcgOut o{OTN_OK, 0, 0.0};
-  if (has_x0) hvp(grid, a, x, rho, a.q, r0, r1, sh, nh);
+  double q = 0.0;
+  if (has_x0) q = hvp(grid, a, x, rho, rPi, r0, r1, sh, nh);
+  double M = 1.0, bi = 0.0, r = 0.0, z = 0.0, p = 0.0;
   double loc[3] = {0.0, 0.0, 0.0};
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += NT) {
-    const double Mi = __dmul_rn(__ldg(a.rP + i), __dsub_rn(1.0, __dmul_rn(rho, __ldg(a.mu + i))));
-    a.M[i] = Mi;
-    const double bi = bvec ? __ldg(bvec + i) : -__ldg(a.g + i);
-    double ri;
+  if (row.own) {
+    M = __dmul_rn(rPi, __dsub_rn(1.0, __dmul_rn(rho, __ldg(a.mu + row.i))));
+    bi = bvec ? __ldg(bvec + row.i) : -__ldg(a.g + row.i);
     if (has_x0) {
-      ri = __dsub_rn(bi, a.q[i]);
+      r = __dsub_rn(bi, q);
     } else {
-      x[i] = 0.0;
-      ri = bi;
+      x = 0.0;
+      r = bi;
     }
-    a.r[i] = ri;
-    const double zi = __ddiv_rn(ri, Mi);
-    a.z[i] = zi;
-    a.p[i] = zi;
-    loc[0] += fabs(ri);
-    loc[1] = fma(ri, zi, loc[1]);
-    if (Mi <= 0.0) loc[2] += 1.0;
+    z = __ddiv_rn(r, M);
+    p = z;
+    loc[0] = fabs(r);
+    loc[1] = fma(r, z, 0.0);
+    if (M <= 0.0) loc[2] = 1.0;
+  } else {
+    x = 0.0;
   }
   grid_reduce<3>(grid, loc, a.red, slot, sh);
   if (loc[2] > 0.0) { o.status = OTN_ST_PRECOND; return o; }
@@ -883,43 +928,40 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, double rho, const
   double rz = loc[1];
   double norm = loc[0];
   for (int64_t k = 1; k <= max_iters; ++k) {
-    hvp(grid, a, a.p, rho, a.q, r0, r1, sh, nh);
-    double pq[1] = {0.0};
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += NT) pq[0] = fma(a.p[i], a.q[i], pq[0]);
+    q = hvp(grid, a, p, rho, rPi, r0, r1, sh, nh);
+    double pq[1] = {fma(p, q, 0.0)};
     grid_reduce<1>(grid, pq, a.red, slot, sh);
     if (pq[0] <= 0.0) { o.status = OTN_ST_BREAKDOWN; o.iters = k; o.resid = pq[0]; return o; }
     const double alpha = rz / pq[0];
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += NT) {
-      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, a.p[i]));
-      a.r[i] = __dsub_rn(a.r[i], __dmul_rn(alpha, a.q[i]));
-    }
+    x = __dadd_rn(x, __dmul_rn(alpha, p));
+    r = __dsub_rn(r, __dmul_rn(alpha, q));
     if (k % kRefresh == 0) {
-      hvp(grid, a, x, rho, a.q, r0, r1, sh, nh);
-      for (int64_t i = r0 + threadIdx.x; i < r1; i += NT) {
-        const double bi = bvec ? __ldg(bvec + i) : -__ldg(a.g + i);
-        a.r[i] = __dsub_rn(bi, a.q[i]);
-      }
+      const double qx = hvp(grid, a, x, rho, rPi, r0, r1, sh, nh);
+      r = __dsub_rn(bi, qx);
     }
-    double nz[2] = {0.0, 0.0};
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += NT) {
-      const double ri = a.r[i];
-      const double zi = __ddiv_rn(ri, a.M[i]);
-      a.z[i] = zi;
-      nz[0] += fabs(ri);
-      nz[1] = fma(ri, zi, nz[1]);
-    }
+    if (!row.own) r = 0.0;
+    z = __ddiv_rn(r, M);
+    double nz[2] = {fabs(r), fma(r, z, 0.0)};
     grid_reduce<2>(grid, nz, a.red, slot, sh);
     norm = nz[0];
     if (norm <= tol) { o.iters = k; o.resid = norm; return o; }
     const double beta = nz[1] / rz;
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += NT)
-      a.p[i] = __dadd_rn(a.z[i], __dmul_rn(beta, a.p[i]));
+    p = __dadd_rn(z, __dmul_rn(beta, p));
     rz = nz[1];
   }
   o.status = OTN_ST_NONCONVERGENCE;
   o.iters = max_iters;
   o.resid = norm;
   return o;
+}
+
+// Column pass of the CTA rows for x held one value per thread (phase A + A2).
+__device__ void column_pass(cg::grid_group& grid, const CoopArgs& a, double xv, int kind,
+                            double* out, int64_t r0, int64_t r1, Smem& sh) {
+  stage_x(xv, sh);
+  phase_a(plan_view(a, r0, r1), r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
+  grid.sync();
+  phase_a2(a, kind, out, sh);
 }
 
 __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
@@ -933,6 +975,8 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
   int64_t nh = 0;
   DevResult res{};
   res.status = OTN_OK;
+  const Row row{int64_t(threadIdx.x) < r1 - r0, r0 + threadIdx.x};
+  const double rPi = row.own && a.rP ? __ldg(a.rP + row.i) : 0.0;
   __syncthreads();
   stage_layout(a, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld);
   if (s_mode == kPlanSparse) stage_sparse(a, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
@@ -951,26 +995,21 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
   }
 
   if (a.mode == kModeNewton) {
-    double gl[1] = {0.0};
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += NT) gl[0] += fabs(__ldg(a.g + i));
+    const double gi = row.own ? __ldg(a.g + row.i) : 0.0;
+    double gl[1] = {fabs(gi)};
     grid_reduce<1>(grid, gl, a.red, slot, sh);
     const double gn = gl[0];
     res.rho_final = a.rho0;
-    if (gn == 0.0) {
-      for (int64_t i = r0 + threadIdx.x; i < r1; i += NT) a.d[i] = 0.0;
-      __syncthreads();
-    } else {
-      for (int64_t i = r0 + threadIdx.x; i < r1; i += NT)
-        a.d[i] = __ddiv_rn(-__ldg(a.g + i), __ldg(a.rP + i));
+    double d = 0.0;
+    if (gn != 0.0) {
+      if (row.own) d = __ddiv_rn(-gi, rPi);
       double rho = a.rho0, used = a.rho0;
       int64_t total = 0;
       const double tol = __dmul_rn(__dmul_rn(0.25, a.eta), gn);
       const double target = __dmul_rn(a.eta, gn);
       while (true) {
-        hvp(grid, a, a.d, 1.0, a.q, r0, r1, sh, nh);
-        double rl[1] = {0.0};
-        for (int64_t i = r0 + threadIdx.x; i < r1; i += NT)
-          rl[0] += fabs(__dadd_rn(a.q[i], __ldg(a.g + i)));
+        const double q = hvp(grid, a, d, 1.0, rPi, r0, r1, sh, nh);
+        double rl[1] = {row.own ? fabs(__dadd_rn(q, gi)) : 0.0};
         grid_reduce<1>(grid, rl, a.red, slot, sh);
         if (rl[0] <= target) { res.resid_l1 = rl[0]; break; }
         if (__dsub_rn(1.0, rho) < 1e-12) {
@@ -980,8 +1019,8 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
           break;
         }
         ++res.pcg_calls;
-        const PcgOut po = pcg(grid, a, rho, nullptr, tol, a.d, a.zero_init == 0, a.max_iters,
-                              r0, r1, slot, sh, nh);
+        const PcgOut po = pcg(grid, a, row, rPi, rho, nullptr, tol, d, a.zero_init == 0,
+                              a.max_iters, r0, r1, slot, sh, nh);
         if (po.status != OTN_OK) {
           res.status = po.status;
           res.diag_rho = rho;
@@ -996,37 +1035,37 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
       res.cg_iters = total;
       res.rho_final = used;
     }
+    if (row.own) a.d[row.i] = d;
     if (res.status == OTN_OK && a.dv) {
-      __syncthreads();
-      phase_a(plan_view(a, r0, r1), a.d, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
-      grid.sync();
-      phase_a2(a, 1, a.dv, sh);
-      double sl[1] = {0.0};
-      for (int64_t i = r0 + threadIdx.x; i < r1; i += NT) sl[0] = fma(__ldg(a.g + i), a.d[i], sl[0]);
+      column_pass(grid, a, d, 1, a.dv, r0, r1, sh);
+      double sl[1] = {fma(gi, d, 0.0)};
       grid_reduce<1>(grid, sl, a.red, slot, sh);
       res.slope = -sl[0];
     }
   } else if (a.mode == kModePcg) {
     res.pcg_calls = 1;
-    const PcgOut po = pcg(grid, a, a.rho, a.b, a.tol, a.d, a.has_x0 != 0, a.max_iters, r0, r1,
-                          slot, sh, nh);
+    double x = row.own && a.has_x0 ? a.d[row.i] : 0.0;
+    const PcgOut po = pcg(grid, a, row, rPi, a.rho, a.b, a.tol, x, a.has_x0 != 0, a.max_iters,
+                          r0, r1, slot, sh, nh);
+    if (row.own) a.d[row.i] = x;
     res.status = po.status;
     res.cg_iters = po.iters;
     res.resid_l1 = po.resid;
     res.diag_rho = a.rho;
     res.diag_resid = po.resid;
   } else if (a.mode == kModeHvp) {
-    hvp(grid, a, a.xin, a.rho, a.d, r0, r1, sh, nh);
+    const double q = hvp(grid, a, row.own ? a.xin[row.i] : 0.0, a.rho, rPi, r0, r1, sh, nh);
+    if (row.own) a.d[row.i] = q;
   } else if (a.mode == kModePc || a.mode == kModeRmatvec) {
-    phase_a(plan_view(a, r0, r1), a.xin, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
-    grid.sync();
-    phase_a2(a, a.mode == kModePc ? 0 : 2, a.wc, sh);
+    column_pass(grid, a, row.own ? a.xin[row.i] : 0.0, a.mode == kModePc ? 0 : 2, a.wc, r0, r1, sh);
     grid.sync();
     for (int64_t i = int64_t(blockIdx.x) * NT + threadIdx.x; i < a.n; i += int64_t(G) * NT)
       a.d[i] = __ldcg(a.wc + i);
   } else if (a.mode == kModeProbe) {
     // Diagnostic: repeat one building block max_iters times (bench tooling).
     const int what = a.has_x0;
+    const double xv = row.own ? a.xin[row.i] : 0.0;
+    stage_x(xv, sh);
     for (int64_t k = 0; k < a.max_iters; ++k) {
       if (what == 0) {
         grid.sync();
@@ -1034,17 +1073,16 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
         double v[2] = {1.0, 2.0};
         grid_reduce<2>(grid, v, a.red, slot, sh);
       } else if (what == 2) {
-        phase_a(plan_view(a, r0, r1), a.xin, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
+        phase_a(plan_view(a, r0, r1), r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
         __syncthreads();
       } else if (what == 3) {
-        phase_b(plan_view(a, r0, r1), a.xin, r0, r1, a.sv, sh);
+        phase_b(plan_view(a, r0, r1), a.xin, r0, r1, sh);
       } else if (what == 4) {
-        phase_a(plan_view(a, r0, r1), a.xin, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
-        grid.sync();
-        phase_a2(a, 0, a.wc, sh);
+        column_pass(grid, a, xv, 0, a.wc, r0, r1, sh);
         grid.sync();
       } else {
-        hvp(grid, a, a.xin, 0.5, a.d, r0, r1, sh, nh);
+        const double q = hvp(grid, a, xv, 0.5, rPi, r0, r1, sh, nh);
+        if (row.own) a.d[row.i] = q;
       }
     }
   } else if (a.mode == kModeMatvec) {
@@ -1052,15 +1090,17 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
     for (int64_t j = int64_t(blockIdx.x) * NT + threadIdx.x; j < a.ld; j += int64_t(G) * NT)
       a.wc[j] = j < a.n ? __ldg(a.xin + j) : 0.0;
     grid.sync();
-    phase_b(plan_view(a, r0, r1), a.wc, r0, r1, a.sv, sh);
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += NT) a.d[i] = a.sv[i];
+    phase_b(plan_view(a, r0, r1), a.wc, r0, r1, sh);
+    if (row.own) a.d[row.i] = sh.sv[threadIdx.x];
   }
   res.hvps = nh;
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.res = res;
 }
 
-constexpr size_t kRingBytes = size_t(kRingDepth) * kSlotBytes;
-constexpr size_t kDynBytes = kRingBytes > kSparseBytes ? kRingBytes : kSparseBytes;
+static_assert(kRingBytes == size_t(kRingDepth) * kSlotBytes, "ring layout");
+constexpr size_t kDynRing = kRingBytes + size_t(kSpanSmem) * 4;
+constexpr size_t kDynSparse = kSparseBytes + size_t(kSparseRows) * 4;
+constexpr size_t kDynBytes = kDynRing > kDynSparse ? kDynRing : kDynSparse;
 
 // ---------------------------------------------------------------------------
 // k_partition: one CTA picks the plan mode of the next k_coop launch and its
@@ -1181,6 +1221,8 @@ __global__ void __launch_bounds__(kPartThreads) k_partition(const uint64_t* mask
 }
 
 cudaError_t launch_coop(otn_ctx* x, const CoopArgs& a0) {
+  // CG vectors live one row per thread: at most NT rows per CTA (n <= 75776 on 148 SMs)
+  if ((a0.n + x->coop_blocks - 1) / x->coop_blocks > NT) return cudaErrorInvalidValue;
   CoopArgs a = a0;
   a.stages = kRingDepth;
   a.part = x->part;

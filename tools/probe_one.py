@@ -21,6 +21,7 @@ x = torch.randn(k.ld, dtype=torch.float64, device="cuda")
 out = k.vec()
 mask = s._mask if masked else None
 for _ in range(3):
-    k.call("otn_probe", vptr(s._P), vptr(mask), vptr(s._cP), vptr(s._rP), vptr(x), vptr(out), what, 20)
+    k.call("otn_probe", vptr(s._P), vptr(mask), vptr(s._cP), vptr(s._rP), vptr(x), vptr(out), what,
+           int(os.environ.get("PROBE_REPS", "20")))
 torch.cuda.synchronize()
 print("coop_launches_before_probe", ncoop)
