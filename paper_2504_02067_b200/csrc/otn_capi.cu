@@ -38,9 +38,19 @@ int fail(int code, const char* what, cudaError_t e = cudaSuccess) {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Wait for the stream by polling: the solver's host decisions wait on one
+// scalar after every short kernel sequence, and a blocking synchronize adds
+// the driver's wake-up latency to each of those round trips.
+cudaError_t stream_wait(cudaStream_t s) {
+  cudaError_t e;
+  while ((e = cudaStreamQuery(s)) == cudaErrorNotReady) {
+  }
+  return e;
+}
+
 int sync_copy(otn_ctx* x, void* host, const void* dev, size_t bytes, const char* what) {
   OTN_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, x->stream), what);
-  OTN_CUDA(cudaStreamSynchronize(x->stream), what);
+  OTN_CUDA(stream_wait(x->stream), what);
   return OTN_OK;
 }
 
@@ -102,7 +112,7 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
     delete x;
     return fail(OTN_ERR_CUDA, "otn_create: persistent solver does not fit on an SM", e);
   }
-  x->coop_blocks = x->num_sms;   // one CTA per SM (co-residency guaranteed)
+  x->coop_blocks = x->num_sms < otn::kRedStride ? x->num_sms : otn::kRedStride;   // one CTA per SM
   {
     // the persistent solver stages each CTA's (row, tile) spans in shared memory
     const int64_t rows = (n + x->coop_blocks - 1) / x->coop_blocks;
@@ -134,7 +144,7 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
   size_t o_t0 = off; off += vec;
   size_t o_t1 = off; off += vec;
   size_t o_wp = off; off += align_up(size_t(x->coop_blocks) * ld * sizeof(double), 256);
-  size_t o_red = off; off += align_up(size_t(otn::kRedSlots) * x->coop_blocks * otn::kRedWidth * sizeof(double), 256);
+  size_t o_red = off; off += align_up(size_t(otn::kRedSlots) * otn::kRedStride * otn::kRedWidth * sizeof(double), 256);
   size_t o_lse = off; off += align_up(size_t(x->lse_slabs) * ld * 2 * sizeof(double), 256);
   size_t o_sc = off; off += align_up(64 * sizeof(double), 256);
   size_t o_fl = off; off += align_up(16 * sizeof(int), 256);
@@ -441,7 +451,7 @@ int otn_reduce_n(otn_ctx* x, int64_t n, int op, const double* a, const double* b
                            x->stream), "otn_reduce_n: copy");
   OTN_CUDA(cudaMemcpyAsync(x->h_flags + 2, x->flags + 2, sizeof(int), cudaMemcpyDeviceToHost,
                            x->stream), "otn_reduce_n: copy");
-  OTN_CUDA(cudaStreamSynchronize(x->stream), "otn_reduce_n: sync");
+  OTN_CUDA(stream_wait(x->stream), "otn_reduce_n: sync");
   host_out[0] = x->h_scal[8];
   host_out[1] = x->h_scal[9];
   if (host_flags) *host_flags = x->h_flags[2];
@@ -467,7 +477,7 @@ int otn_reduce(otn_ctx* x, int op, const double* a, const double* b, const doubl
                            x->stream), "otn_reduce: copy");
   OTN_CUDA(cudaMemcpyAsync(x->h_flags + 2, x->flags + 2, sizeof(int), cudaMemcpyDeviceToHost,
                            x->stream), "otn_reduce: copy");
-  OTN_CUDA(cudaStreamSynchronize(x->stream), "otn_reduce: sync");
+  OTN_CUDA(stream_wait(x->stream), "otn_reduce: sync");
   host_out[0] = x->h_scal[8];
   host_out[1] = x->h_scal[9];
   if (host_flags) *host_flags = x->h_flags[2];
@@ -483,7 +493,7 @@ int otn_round_plan(otn_ctx* x, double* P, const double* C, const double* r, cons
                            cudaMemcpyDeviceToHost, x->stream), "otn_round_plan: copy");
   OTN_CUDA(cudaMemcpyAsync(x->h_flags + 3, x->flags + 3, sizeof(int), cudaMemcpyDeviceToHost,
                            x->stream), "otn_round_plan: copy");
-  OTN_CUDA(cudaStreamSynchronize(x->stream), "otn_round_plan: sync");
+  OTN_CUDA(stream_wait(x->stream), "otn_round_plan: sync");
   host_out[0] = x->h_scal[16 + 3];   // primal <P, C>
   host_out[1] = x->h_scal[16 + 2];   // deficit
   if (host_flags) *host_flags = x->h_flags[3];

@@ -12,7 +12,8 @@ constexpr int kCoopThreads = 512;       // one CTA per SM for the persistent sol
 constexpr int kLseThreads = 256;        // 8 warps: one row per warp
 constexpr int kColTile = 64;            // columns per CTA in column reductions
 constexpr int kRedSlots = 2;            // rotating grid-reduction slots
-constexpr int kRedWidth = 4;            // doubles per CTA per slot
+constexpr int kRedWidth = 4;            // values per grid reduction (at most)
+constexpr int kRedStride = 256;         // CTA partials per value (>= persistent-solver CTAs)
 constexpr int kSegCols = 64;            // plan segment (zero-skip granularity): 64 cols = 512 B
 constexpr int kSegWordCols = 64 * kSegCols;  // columns covered by one 64-bit mask word
 

@@ -370,7 +370,7 @@ class DualState:
 
     def _system(self):
         from .newton import DiscountedSystem
-        return DiscountedSystem.from_state(self)
+        return DiscountedSystem.from_state(self, check_flags=False)   # the Newton launch checks
 
     def _dir_bufs(self):
         bufs = getattr(self, "_dirbufs", None)

@@ -83,9 +83,14 @@ class DiscountedSystem:
         self._mu_counted = False
 
     @classmethod
-    def from_state(cls, state):
+    def from_state(cls, state, check_flags=True):
         """Snapshot the current plan (newton.py:81-90): rP, cP from the log-domain
-        caches, P into the state's reusable buffer, mu fused into that pass."""
+        caches, P into the state's reusable buffer, mu fused into that pass.
+
+        check_flags=False skips the host round trip for the overflow /
+        nonpositive-sum flags: the persistent solver reads them first and
+        returns the same statuses (same order), so the projector's Newton
+        launch raises the same errors without an extra synchronization."""
         ctx = state._ctx
         bufs = getattr(state, "_sysbufs", None)
         if bufs is None:
@@ -95,12 +100,13 @@ class DiscountedSystem:
         lr, lc = state._lr_dev(), state._lc_dev()
         ctx.call("otn_system_prep", vptr(lr), vptr(lc), vptr(rP), vptr(cP), vptr(icP), None)
         P, mask = state._materialize(reuse_buffer=True, icP=icP, rP=rP, mu=mu, check=False)
-        flags = (ctypes.c_int * 4)()
-        ctx.call("otn_read_flags", flags)
-        if flags[0]:
-            _lib.raise_for_status(_lib.OTN_ST_PLAN_OVERFLOW, "materialize_plan")
-        if flags[1]:
-            _lib.raise_for_status(_lib.OTN_ST_NONPOSITIVE_SUMS, "DiscountedSystem")
+        if check_flags:
+            flags = (ctypes.c_int * 4)()
+            ctx.call("otn_read_flags", flags)
+            if flags[0]:
+                _lib.raise_for_status(_lib.OTN_ST_PLAN_OVERFLOW, "materialize_plan")
+            if flags[1]:
+                _lib.raise_for_status(_lib.OTN_ST_NONPOSITIVE_SUMS, "DiscountedSystem")
         return cls(P, rP, cP, _ctx=ctx, _mu=mu, _icP=icP, _mask=mask)
 
     # -- host views for API parity ---------------------------------------------
