@@ -9,6 +9,10 @@
 
 namespace otn {
 
+// One warp per row: 2-warp blocks spread the n warps evenly over the SMs
+// (256-thread blocks left some SMs a whole block behind: 3 vs 4 per SM at n=4096).
+constexpr int kRowThreads = 64;
+
 struct LseArgs {
   const double* C;
   int64_t n, ld;
@@ -39,40 +43,53 @@ __device__ __forceinline__ double finish(const LseArgs& a, int64_t j, double lse
 // per step, keeps an online (max, sum-exp) pair and rescales at most once per
 // step, so the cost is ~1.1 exp per entry.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kLseThreads) k_lse_rows(LseArgs a) {
+__global__ void __launch_bounds__(kRowThreads) k_lse_rows(LseArgs a) {
+  __shared__ double2 s_exp[64];
+  exp_tab_load(s_exp);
+  __syncthreads();
   const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= a.n) return;
   const double* crow = a.C + row * a.ld;
   const int64_t n = a.n;
   double m = OTN_NINF, s = 0.0;
+  // the next step's four 16-byte C loads are issued before this step's math
+  // (the inner vector is L1-resident and loaded in place); j + 1 < ld always
+  double2 cur[4], nxt[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t j = 64 * k + 2 * lane;
+    cur[k] = j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
+  }
   for (int64_t base = 0; base < n; base += 256) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t j = base + 256 + 64 * k + 2 * lane;
+      nxt[k] = j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
+    }
     double b[8];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t j = base + 64 * k + 2 * lane;
-      if (j < n) {
-        const double2 c = ld_stream2(crow + j);
-        b[2 * k] = __dadd_rn(__dmul_rn(a.ng, c.x), eff(a.inner, a.inner_d, a.alpha, j));
-        b[2 * k + 1] = (j + 1 < n)
-            ? __dadd_rn(__dmul_rn(a.ng, c.y), eff(a.inner, a.inner_d, a.alpha, j + 1))
-            : OTN_NINF;
-      } else {
-        b[2 * k] = OTN_NINF;
-        b[2 * k + 1] = OTN_NINF;
-      }
+      b[2 * k] = j < n ? __dadd_rn(__dmul_rn(a.ng, cur[k].x), eff(a.inner, a.inner_d, a.alpha, j))
+                       : OTN_NINF;
+      b[2 * k + 1] = j + 1 < n
+          ? __dadd_rn(__dmul_rn(a.ng, cur[k].y), eff(a.inner, a.inner_d, a.alpha, j + 1))
+          : OTN_NINF;
     }
     double cm = b[0];
 #pragma unroll
     for (int k = 1; k < 8; ++k) cm = fmax(cm, b[k]);
     if (cm > m) {
-      s = s * exp_fast(m - cm);
+      s = s * exp_tab(m - cm, s_exp);
       m = cm;
     }
     if (m != OTN_NINF) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) s += exp_fast(b[k] - m);
+      for (int k = 0; k < 8; ++k) s += exp_tab(b[k] - m, s_exp);
     }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cur[k] = nxt[k];
   }
   warp_lse(m, s);
   if (lane == 0) a.out[row] = finish(a, row, lse_value(m, s));
@@ -88,6 +105,9 @@ __global__ void __launch_bounds__(kLseThreads) k_lse_cols_part(LseArgs a, int64_
                                                                double* part) {
   __shared__ double sm_m[8][kColTile];
   __shared__ double sm_s[8][kColTile];
+  __shared__ double2 s_exp[64];
+  exp_tab_load(s_exp);
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t j = int64_t(blockIdx.x) * kColTile + 2 * lane;
   const int64_t i0 = int64_t(blockIdx.y) * slab_rows;
@@ -111,15 +131,15 @@ __global__ void __launch_bounds__(kLseThreads) k_lse_cols_part(LseArgs a, int64_
     }
     double cm0 = fmax(fmax(b0[0], b0[1]), fmax(b0[2], b0[3]));
     double cm1 = fmax(fmax(b1[0], b1[1]), fmax(b1[2], b1[3]));
-    if (cm0 > m0) { s0 = s0 * exp_fast(m0 - cm0); m0 = cm0; }
-    if (cm1 > m1) { s1 = s1 * exp_fast(m1 - cm1); m1 = cm1; }
+    if (cm0 > m0) { s0 = s0 * exp_tab(m0 - cm0, s_exp); m0 = cm0; }
+    if (cm1 > m1) { s1 = s1 * exp_tab(m1 - cm1, s_exp); m1 = cm1; }
     if (m0 != OTN_NINF) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) s0 += exp_fast(b0[k] - m0);
+      for (int k = 0; k < 4; ++k) s0 += exp_tab(b0[k] - m0, s_exp);
     }
     if (m1 != OTN_NINF) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) s1 += exp_fast(b1[k] - m1);
+      for (int k = 0; k < 4; ++k) s1 += exp_tab(b1[k] - m1, s_exp);
     }
   }
   sm_m[warp][2 * lane] = m0;
@@ -153,13 +173,16 @@ __global__ void k_lse_cols_fin(LseArgs a, int slabs, const double* part) {
 }
 
 // ---------------------------------------------------------------------------
-// Plan: P_ij = exp_fast((ng*C_ij + v_j) + u_i), one warp per row, 16-byte stores,
+// Plan: P_ij = exp_tab((ng*C_ij + v_j) + u_i), one warp per row, 16-byte stores,
 // zeros in the padding columns.  Fused K5: mu_i = (sum_j P_ij^2 icP_j)/rP_i.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kLseThreads) k_materialize(const double* __restrict__ C,
+__global__ void __launch_bounds__(kRowThreads) k_materialize(const double* __restrict__ C,
     int64_t n, int64_t ld, double ng, const double* __restrict__ u, const double* __restrict__ v,
     double* __restrict__ P, const double* __restrict__ icP, const double* __restrict__ rP,
     double* __restrict__ mu, int* __restrict__ flag, uint64_t* __restrict__ mask) {
+  __shared__ double2 s_exp[64];
+  exp_tab_load(s_exp);
+  __syncthreads();
   const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
@@ -170,7 +193,23 @@ __global__ void __launch_bounds__(kLseThreads) k_materialize(const double* __res
   double acc = 0.0, mx = OTN_NINF;
   uint64_t bits = 0;
   int nnz = 0;
+  // one 256-column step per iteration, its loads issued one step ahead
+  double2 cc[4], cn[4];
+  double vc[8], vn[8], ic[8], inx[8];
+  auto load = [&](int64_t base, double2 (&c)[4], double (&vv)[8], double (&ii)[8]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t j = base + 64 * k + 2 * lane;
+      c[k] = j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
+      vv[2 * k] = j < n ? __ldg(v + j) : 0.0;
+      vv[2 * k + 1] = j + 1 < n ? __ldg(v + j + 1) : 0.0;
+      ii[2 * k] = icP && j < n ? __ldg(icP + j) : 0.0;
+      ii[2 * k + 1] = icP && j + 1 < n ? __ldg(icP + j + 1) : 0.0;
+    }
+  };
+  load(0, cc, vc, ic);
   for (int64_t base = 0; base < ld; base += 256) {
+    if (base + 256 < ld) load(base + 256, cn, vn, inx);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t j = base + 64 * k + 2 * lane;
@@ -178,18 +217,17 @@ __global__ void __launch_bounds__(kLseThreads) k_materialize(const double* __res
       if (j < ld) {
         double e0 = OTN_NINF, e1 = OTN_NINF;
         if (j < n) {
-          const double2 c = ld_stream2(crow + j);
-          e0 = __dadd_rn(__dadd_rn(__dmul_rn(ng, c.x), __ldg(v + j)), ui);
-          if (j + 1 < n) e1 = __dadd_rn(__dadd_rn(__dmul_rn(ng, c.y), __ldg(v + j + 1)), ui);
+          e0 = __dadd_rn(__dadd_rn(__dmul_rn(ng, cc[k].x), vc[2 * k]), ui);
+          if (j + 1 < n) e1 = __dadd_rn(__dadd_rn(__dmul_rn(ng, cc[k].y), vc[2 * k + 1]), ui);
         }
         mx = fmax(mx, fmax(e0, e1));
-        const double p0 = exp_fast(e0), p1 = exp_fast(e1);
+        const double p0 = exp_tab(e0, s_exp), p1 = exp_tab(e1, s_exp);
         *reinterpret_cast<double2*>(prow + j) = make_double2(p0, p1);
         nz = (p0 != 0.0) || (p1 != 0.0);
         nnz += int(p0 != 0.0) + int(p1 != 0.0);
         if (icP) {
-          if (j < n) acc = fma(__dmul_rn(p0, p0), __ldg(icP + j), acc);
-          if (j + 1 < n) acc = fma(__dmul_rn(p1, p1), __ldg(icP + j + 1), acc);
+          if (j < n) acc = fma(__dmul_rn(p0, p0), ic[2 * k], acc);
+          if (j + 1 < n) acc = fma(__dmul_rn(p1, p1), ic[2 * k + 1], acc);
         }
       }
       // segment (64 columns = 512 B) occupancy bit for the HVP's zero skipping
@@ -199,6 +237,10 @@ __global__ void __launch_bounds__(kLseThreads) k_materialize(const double* __res
       if (lane == 0) mask[row * mw + base / kSegWordCols] = bits;
       bits = 0;
     }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cc[k] = cn[k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { vc[k] = vn[k]; ic[k] = inx[k]; }
   }
   mx = warp_max(mx);
   if (icP) acc = warp_sum(acc);
@@ -272,15 +314,15 @@ __global__ void __launch_bounds__(kLseThreads) k_square_matvec(const double* __r
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-static inline unsigned rows_grid(int64_t n) {
-  return unsigned((n + (kLseThreads / 32) - 1) / (kLseThreads / 32));
+static inline unsigned rows_grid(int64_t n, int threads = kLseThreads) {
+  return unsigned((n + (threads / 32) - 1) / (threads / 32));
 }
 
 cudaError_t launch_lse_rows(otn_ctx* x, const double* C, double ng, const double* outer,
                             const double* outer_d, const double* inner, const double* inner_d,
                             double alpha, int mode, double* out) {
   LseArgs a{C, x->n, x->ld, ng, outer, outer_d, inner, inner_d, alpha, mode, out};
-  k_lse_rows<<<rows_grid(x->n), kLseThreads, 0, x->stream>>>(a);
+  k_lse_rows<<<rows_grid(x->n, kRowThreads), kRowThreads, 0, x->stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -299,7 +341,7 @@ cudaError_t launch_lse_cols(otn_ctx* x, const double* C, double ng, const double
 cudaError_t launch_materialize(otn_ctx* x, const double* C, double ng, const double* u,
                                const double* v, double* P, const double* icP, const double* rP,
                                double* mu, int* flag, uint64_t* mask) {
-  k_materialize<<<rows_grid(x->n), kLseThreads, 0, x->stream>>>(C, x->n, x->ld, ng, u, v, P, icP,
+  k_materialize<<<rows_grid(x->n, kRowThreads), kRowThreads, 0, x->stream>>>(C, x->n, x->ld, ng, u, v, P, icP,
                                                                  rP, mu, flag, mask);
   return cudaGetLastError();
 }

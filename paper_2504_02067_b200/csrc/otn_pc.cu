@@ -43,6 +43,8 @@ __global__ void __launch_bounds__(kPcThreads, 2) k_pair(PairArgs p) {
   __shared__ double sb[kPcMaxDim][kPcTile];
   __shared__ double scp[kPcTile];
   __shared__ double svec[kPcTile];
+  __shared__ double2 s_exp[64];
+  exp_tab_load(s_exp);                               // made visible by the tile loop's barrier
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t i0 = (int64_t(blockIdx.x) * 8 + warp) * RW;
   double a[RW][kPcMaxDim], rp[RW];
@@ -98,12 +100,12 @@ __global__ void __launch_bounds__(kPcThreads, 2) k_pair(PairArgs p) {
           cm = fmax(cm, e[q]);
         }
         if (cm > m[r]) {
-          s[r] = s[r] * exp_fast(m[r] - cm);
+          s[r] = s[r] * exp_tab(m[r] - cm, s_exp);
           m[r] = cm;
         }
         if (m[r] != OTN_NINF) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) s[r] += exp_fast(e[q] - m[r]);
+          for (int q = 0; q < 8; ++q) s[r] += exp_tab(e[q] - m[r], s_exp);
         }
       }
     } else {
@@ -123,7 +125,7 @@ __global__ void __launch_bounds__(kPcThreads, 2) k_pair(PairArgs p) {
             const double kc = __dmul_rn(p.ng, c);
             const double e = p.order == 0 ? __dadd_rn(__dadd_rn(kc, cpj), rp[r])
                                           : __dadd_rn(__dadd_rn(kc, rp[r]), cpj);
-            const double pe = exp_fast(e);
+            const double pe = exp_tab(e, s_exp);
             if (OP == OTN_PC_DOT) {
               s[r] = fma(pe, vj, s[r]);
             } else if (OP == OTN_PC_DOTC) {

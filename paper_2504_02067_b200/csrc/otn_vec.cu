@@ -10,6 +10,11 @@ namespace otn {
 // ---------------------------------------------------------------------------
 __global__ void k_vec(int op, int64_t n, double s, const double* a, const double* b,
                       const double* c, const double* d, double* out) {
+  __shared__ double2 s_exp[64];
+  if (op == OTN_VEC_EXP) {                          // uniform: the table only where it is used
+    exp_tab_load(s_exp);
+    __syncthreads();
+  }
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     double o;
@@ -20,7 +25,7 @@ __global__ void k_vec(int op, int64_t n, double s, const double* a, const double
         o = __dadd_rn(__dadd_rn(a[i], __dmul_rn(s, b[i])), __dsub_rn(c[i], d[i]));
         break;
       case OTN_VEC_EXTRAP: o = __dadd_rn(a[i], __dmul_rn(s, __dsub_rn(a[i], b[i]))); break;
-      case OTN_VEC_EXP: o = exp_fast(a[i]); break;
+      case OTN_VEC_EXP: o = exp_tab(a[i], s_exp); break;
       case OTN_VEC_GRAD: o = __dsub_rn(exp_fast(a[i]), b[i]); break;
       case OTN_VEC_MUL_SUB: o = __dsub_rn(__dmul_rn(a[i], b[i]), __dmul_rn(s, c[i])); break;
       case OTN_VEC_DIV: o = __ddiv_rn(a[i], b[i]); break;

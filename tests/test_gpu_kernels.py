@@ -184,9 +184,12 @@ def test_rho_anneals_on_quarter_grid():
     assert np.abs(resid).sum() <= 0.01 * np.abs(grad).sum() + 1e-15
 
 
-def test_exp_fast_accuracy():
-    """The kernels' branch-free exp vs numpy: <= 1 ulp over the whole range,
-    exact 0 / inf / NaN at the ends (used for every plan entry)."""
+@pytest.mark.parametrize("op", ["VEC_EXP", "VEC_GRAD"])
+def test_exp_fast_accuracy(op):
+    """The kernels' two branch-free exps vs numpy: <= 1 ulp over the whole
+    range, exact 0 / inf / NaN at the ends.  VEC_EXP runs exp_tab (the
+    table-driven exp of every LSE / plan / pair entry); VEC_GRAD with b = 0
+    runs exp_fast (the polynomial one used for O(n) work and LSE merges)."""
     import torch
     from paper_2504_02067_b200 import _lib
     from paper_2504_02067_b200._device import Context, require_cuda, vptr
@@ -202,7 +205,8 @@ def test_exp_fast_accuracy():
     for k in range(0, x.size, n):
         a = ctx.vec(x[k:k + n])
         out = ctx.vec()
-        ctx.call("otn_vec", _lib.VEC_EXP, 0.0, vptr(a), None, None, None, vptr(out))
+        zero = ctx.vec(np.zeros(n))
+        ctx.call("otn_vec", getattr(_lib, op), 0.0, vptr(a), vptr(zero), None, None, vptr(out))
         got[k:k + n] = ctx.download(out)
     want = np.exp(x)
     both_nan = np.isnan(got) & np.isnan(want)
