@@ -3,7 +3,8 @@ at n = 2^20 (3-D uniform points) on ONE GPU -- the exact-C_max pass, a row
 LSE pass, a row P.w pass, a column LSE pass.  A D5 solve is ~230 such passes
 (D4's call pattern); on G GPUs each pass splits by rows with one n-vector
 allreduce per column product (8 MB at n = 2^20, ~10-20 us over NVLink), so
-the per-pass time over G is the scaling model.  Writes profiles/r01_d5_pass.json."""
+the per-pass time over G is the scaling model.  Writes gpurun_out/r01_d5_pass.json
+(kept as profiles/r01_d5_pass.json)."""
 import json
 import os
 import sys
@@ -48,4 +49,5 @@ res["model"] = {"passes_per_solve_d4_pattern": passes, "solve_1gpu_s": passes * 
                 "solve_8gpu_s_compute_only": passes * per / 8}
 print(json.dumps(res, indent=1))
 os.makedirs("profiles", exist_ok=True)
-json.dump(res, open("profiles/r01_d5_pass.json", "w"), indent=1)
+os.makedirs("gpurun_out", exist_ok=True)
+json.dump(res, open("gpurun_out/r01_d5_pass.json", "w"), indent=1)   # copied to profiles/
