@@ -17,12 +17,13 @@ import numpy as np
 
 from . import _lib, opcount
 from ._device import TELEMETRY, Context, is_tensor, require_cuda, torch, vptr
-from .errors import ConditioningError, NonconvergenceError, StagnationError
+from .errors import ConditioningError, NonconvergenceError, RefusalError, StagnationError
 
 RHO_CAP = 1e-12               # newton.py:32
 RHO_DECAY = 4.0               # newton.py:34
 CG_TOL_FRACTION = 0.25        # newton.py:36
 TRUE_RESIDUAL_REFRESH = 50    # newton.py:38 (compiled into the kernel)
+LAMBDA2_MAX_N = 2048          # newton.py:40
 
 
 @dataclass
@@ -284,3 +285,79 @@ def next_rho0(rho_old):
     if not 0.0 <= rho_old < 1.0:
         raise ConditioningError(f"rho_old must be in [0, 1), got {rho_old}")
     return max(0.0, 1.0 - (1.0 - rho_old) * RHO_DECAY)
+
+
+def lambda2(sys, tol=1e-13):
+    """Second-largest eigenvalue of P_rc (newton.py:220-236).
+
+    The reference eigendecomposes the dense symmetric form
+    S = D(rP)^-1/2 P D(cP)^-1 P^T D(rP)^-1/2 (similar to P_rc).  Here S is
+    never formed: Lanczos with full reorthogonalization runs on the device
+    operators (S x = D(rP)^-1/2 P ((P^T D(rP)^-1/2 x) / cP): one apply_pc and
+    one matvec launch per step), restarting from a fresh vector orthogonal to
+    the basis if the Krylov space closes, until the two largest Ritz values'
+    residual bounds are below ``tol`` (or the basis spans R^n, where they are
+    exact).  Same guard, leading-eigenvalue check and clamp as the reference.
+    """
+    n = sys.n
+    if n > LAMBDA2_MAX_N:
+        raise RefusalError(f"lambda2 needs a dense eigensolve; n={n} exceeds {LAMBDA2_MAX_N}")
+    t = torch()
+    k = sys._ctx
+    isr = 1.0 / t.sqrt(sys._rP[:n])
+    w = k.vec()
+    s_vec = k.vec()
+    xin = k.vec()
+
+    def apply_S(x):
+        xin[:n] = x * isr
+        k.call("otn_apply_pc", vptr(sys._P), vptr(sys._mask), vptr(sys._cP), vptr(xin), vptr(w))
+        k.call("otn_matvec", vptr(sys._P), vptr(sys._mask), vptr(w), vptr(s_vec))
+        return s_vec[:n] * isr
+
+    gen = t.Generator(device=k.device).manual_seed(2504)
+    Q = t.zeros((n, n), dtype=t.float64, device=k.device)
+    alphas, betas = [], []
+    q = t.rand(n, dtype=t.float64, device=k.device, generator=gen) + 0.5
+    q /= t.linalg.vector_norm(q)
+    m = 0
+    evals = np.zeros(1)
+    while m < n:
+        Q[:, m] = q
+        r = apply_S(q)
+        a = float(t.dot(q, r))
+        r -= a * q
+        if m > 0 and betas[-1] > 0.0:
+            r -= betas[-1] * Q[:, m - 1]
+        for _ in range(2):                         # full reorthogonalization (twice is enough)
+            r -= Q[:, : m + 1] @ (Q[:, : m + 1].T @ r)
+        alphas.append(a)
+        b = float(t.linalg.vector_norm(r))
+        m += 1
+        T = np.diag(alphas) + np.diag(betas[: m - 1], 1) + np.diag(betas[: m - 1], -1)
+        evals, vecs = np.linalg.eigh(T)
+        scale = max(abs(evals[-1]), 1.0)
+        if m == n:
+            break
+        if m >= 2 and b * max(abs(vecs[-1, -1]), abs(vecs[-1, -2])) <= tol * scale and m >= min(n, 8):
+            break
+        if b <= 1e-14 * scale:                     # invariant subspace: restart orthogonally
+            betas.append(0.0)
+            for _ in range(10):
+                q = t.rand(n, dtype=t.float64, device=k.device, generator=gen) - 0.5
+                for _ in range(2):
+                    q -= Q[:, :m] @ (Q[:, :m].T @ q)
+                nq = float(t.linalg.vector_norm(q))
+                if nq > 1e-8:
+                    break
+            q = q / nq
+        else:
+            betas.append(b)
+            q = r / b
+    opcount.add(2 * m)
+    lead = float(evals[-1])
+    if abs(lead - 1.0) > 1e-8:
+        raise ConditioningError(f"leading eigenvalue of P_rc is {lead}, expected 1")
+    if n == 1:
+        return 0.0
+    return float(min(evals[-2], 1.0 - 1e-16))

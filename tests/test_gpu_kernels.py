@@ -268,3 +268,42 @@ def test_hvp_plan_modes(n, per_row, heavy, mode):
     x, _ = pcg_solve(sysd, 0.9, -d, 1e-10 * np.abs(d).sum())
     F = np.diag(rP) - 0.9 * (P / cP) @ P.T
     np.testing.assert_allclose(F @ x, -d, rtol=1e-6, atol=1e-9 * np.abs(d).max())
+
+
+class TestLambda2:
+    """lambda2 (newton.py:220-236) by device Lanczos vs the reference's dense
+    eigensolve (test_newton.py:258-283 idioms)."""
+
+    def test_independence_is_rank_one(self):
+        from paper_2504_02067_b200 import lambda2
+        r, c = np.array([0.25, 0.35, 0.4]), np.array([0.3, 0.3, 0.4])
+        P = np.outer(r, c)
+        sysd = DiscountedSystem(P, P.sum(1), P.sum(0))
+        assert lambda2(sysd) == pytest.approx(0.0, abs=1e-10)
+
+    @pytest.mark.parametrize("n,seed", [(10, 60), (64, 1), (700, 2)])
+    def test_matches_dense_eigh(self, n, seed):
+        from paper_2504_02067_b200 import lambda2
+        rng = np.random.default_rng(seed)
+        P = rng.random((n, n)) ** 4
+        P /= P.sum()
+        rP, cP = P.sum(1), P.sum(0)
+        G = P / (np.sqrt(rP)[:, None] * np.sqrt(cP)[None, :])
+        ev = np.linalg.eigvalsh(G @ G.T)
+        assert ev[-1] == pytest.approx(1.0, abs=1e-10)
+        assert lambda2(DiscountedSystem(P, rP, cP)) == pytest.approx(ev[-2], abs=1e-9)
+
+    def test_near_decoupled_blocks_push_lambda2_to_one(self):
+        from paper_2504_02067_b200 import lambda2
+        A = np.full((2, 2), 0.25)
+        eps = 1e-8
+        P = np.block([[A, np.full((2, 2), eps)], [np.full((2, 2), eps), A]])
+        assert lambda2(DiscountedSystem(P, P.sum(axis=1), P.sum(axis=0))) > 1.0 - 1e-6
+
+    def test_size_guard(self):
+        from paper_2504_02067_b200 import lambda2
+        from paper_2504_02067_b200.errors import RefusalError
+        n = 2049
+        P = np.full((n, n), 1.0 / (n * n))
+        with pytest.raises(RefusalError):
+            lambda2(DiscountedSystem(P, P.sum(axis=1), P.sum(axis=0)))
