@@ -153,6 +153,13 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
   x->ws_bytes = off;
   e = cudaMalloc(&x->ws, off);
   if (e != cudaSuccess) { delete x; return fail(OTN_ERR_CUDA, "otn_create: cudaMalloc", e); }
+  // compressed-rows buffer of the global sparse plan mode (one tile, and large
+  // enough that a CTA's nonzeros can outgrow shared memory)
+  x->sg = nullptr;
+  if (ld <= 4096 && n >= 1024) {
+    e = cudaMalloc(&x->sg, size_t(x->coop_blocks) * otn::sparse_g_bytes_per_cta());
+    if (e != cudaSuccess) { cudaFree(x->ws); delete x; return fail(OTN_ERR_CUDA, "otn_create: sparse buffer", e); }
+  }
   cudaMemset(x->ws, 0, off);
   char* base = static_cast<char*>(x->ws);
   x->r = (double*)(base + o_r);
@@ -184,6 +191,7 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
 int otn_destroy(otn_ctx* x) {
   if (!x) return OTN_OK;
   if (x->ws) cudaFree(x->ws);
+  if (x->sg) cudaFree(x->sg);
   if (x->h_scal) cudaFreeHost(x->h_scal);
   if (x->h_flags) cudaFreeHost(x->h_flags);
   if (x->h_res) cudaFreeHost(x->h_res);

@@ -121,8 +121,11 @@ __shared__ int s_win_lo[kMaxTiles], s_win_hi[kMaxTiles];
 //   kPlanL2      the masked plan (sum of row spans) fits in L2: register-
 //                batched direct loads;
 //   kPlanSparse  each CTA compresses its rows' nonzeros into shared memory
-//                once per launch (CSR for P w, a local CSC for P^T x).
-enum PlanMode { kPlanRing = 0, kPlanL2 = 1, kPlanSparse = 2 };
+//                once per launch (CSR for P w, a local CSC for P^T x);
+//   kPlanSparseG the same compressed rows in a per-CTA slice of global memory
+//                (L2-resident) when they exceed shared memory; the CSC then
+//                holds the values themselves (contiguous reads, no gather).
+enum PlanMode { kPlanRing = 0, kPlanL2 = 1, kPlanSparse = 2, kPlanSparseG = 3 };
 __shared__ int s_mode;
 __shared__ int s_nzc;                               // kPlanSparse: nonempty columns of the CTA
 __shared__ int s_split;                             // kPlanSparse: threads splitting the CSC entries
@@ -139,6 +142,7 @@ struct PlanView {
   int nt;                   // tiles
   int mode;                 // PlanMode
   uint32_t* span;           // staged spans: lo | hi << 16, relative to the tile
+  void* sg;                 // kPlanSparseG buffer
 };
 
 // Plans too large for L2 (kPlanRing: streamed from HBM) use a per-thread
@@ -166,7 +170,8 @@ constexpr size_t kSparseBytes = kSparsePerm + size_t(kSparseCap) * 2;
 __device__ __forceinline__ uint32_t* span_base(int mode) {
   char* b = reinterpret_cast<char*>(s_ring);
   return reinterpret_cast<uint32_t*>(b + (mode == kPlanRing ? kRingBytes
-                                          : mode == kPlanSparse ? kSparseBytes : 0));
+                                          : mode == kPlanSparse ? kSparseBytes
+                                          : mode == kPlanSparseG ? kSparseVal : 0));
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -216,6 +221,7 @@ __device__ PlanView plan_view(const CoopArgs& a, int64_t r0, int64_t r1) {
   v.nt = ntiles_of(a.ld);
   v.mode = s_mode;
   v.span = span_base(v.mode);
+  v.sg = a.sg;
   return v;
 }
 
@@ -356,19 +362,46 @@ struct SparseView {
   double* xs;
   int* rp;
   int* cst;
-  double* val;
+  double* val;                                      // CSR values (row-major, columns ascending)
   uint16_t* col;
-  uint16_t* row;
-  uint16_t* perm;
+  uint16_t* row;                                    // row of each CSR entry (build / mode 2)
+  uint16_t* perm;                                   // mode 2: CSC order -> CSR entry
+  double* cval;                                     // mode 3: CSC values
+  uint16_t* crow;                                   // mode 3: CSC rows
+  bool direct;                                      // mode 3
 };
 
-__device__ __forceinline__ SparseView sparse_view() {
+// Per-CTA slice of the global compressed-rows buffer (kPlanSparseG):
+// val, cval [cap] doubles, then col, row, crow [cap] u16.
+constexpr int kSparseGCap = 49152;                  // nonzeros per CTA (u16 CSC offsets)
+constexpr int kSparseGSlot = kSparseGCap + kCoopThreads;   // interleaved CSC: + one row of padding
+constexpr size_t kSparseGBytes = size_t(kSparseGCap) * (8 + 2 + 2) + size_t(kSparseGSlot) * (8 + 2);
+
+__device__ __forceinline__ SparseView sparse_view(void* sg) {
   char* b = reinterpret_cast<char*>(s_ring);
-  return SparseView{reinterpret_cast<double*>(b + kSparseXs), reinterpret_cast<int*>(b + kSparseRp),
-                    reinterpret_cast<int*>(b + kSparseCst), reinterpret_cast<double*>(b + kSparseVal),
-                    reinterpret_cast<uint16_t*>(b + kSparseCol),
-                    reinterpret_cast<uint16_t*>(b + kSparseRow),
-                    reinterpret_cast<uint16_t*>(b + kSparsePerm)};
+  SparseView v;
+  v.xs = reinterpret_cast<double*>(b + kSparseXs);
+  v.rp = reinterpret_cast<int*>(b + kSparseRp);
+  v.cst = reinterpret_cast<int*>(b + kSparseCst);
+  if (s_mode == kPlanSparseG) {
+    char* g = reinterpret_cast<char*>(sg) + size_t(blockIdx.x) * kSparseGBytes;
+    v.val = reinterpret_cast<double*>(g);
+    v.cval = v.val + kSparseGCap;
+    v.col = reinterpret_cast<uint16_t*>(v.cval + kSparseGSlot);
+    v.row = v.col + kSparseGCap;
+    v.crow = v.row + kSparseGCap;
+    v.perm = nullptr;
+    v.direct = true;
+  } else {
+    v.val = reinterpret_cast<double*>(b + kSparseVal);
+    v.col = reinterpret_cast<uint16_t*>(b + kSparseCol);
+    v.row = reinterpret_cast<uint16_t*>(b + kSparseRow);
+    v.perm = reinterpret_cast<uint16_t*>(b + kSparsePerm);
+    v.cval = nullptr;
+    v.crow = nullptr;
+    v.direct = false;
+  }
+  return v;
 }
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
@@ -406,7 +439,7 @@ __device__ void block_incl_scan(int* a, int len, Smem& sh) {
 
 // Extract this CTA's nonzeros (CSR, column order) and build the local CSC.
 __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* wrow, Smem& sh) {
-  const SparseView sp = sparse_view();
+  const SparseView sp = sparse_view(a.sg);
   const PlanView v = plan_view(a, r0, r1);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int rows = int(r1 - r0);
@@ -459,20 +492,52 @@ __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* 
   for (int e = t; e < E; e += NT) atomicAdd(&sp.cst[sp.col[e] - ulo], 1);
   __syncthreads();
   block_incl_scan(sp.cst, W, sh);                   // cst[d] = end of column d
-  // place entries (slot order within a column is arbitrary here), ...
-  for (int e = t; e < E; e += NT) sp.perm[atomicSub(&sp.cst[sp.col[e] - ulo], 1) - 1] = uint16_t(e);
-  __syncthreads();
-  if (t == 0) sp.cst[W] = E;                        // cst[d] = start of column d
-  __syncthreads();
-  // ... then sort each column by entry index = by row (CSR is row-major):
-  // the rows-ascending order of the dense phase A, independent of the atomics.
-  for (int d = t; d < W; d += NT) {
-    const int k0 = sp.cst[d], k1 = sp.cst[d + 1];
-    for (int k = k0 + 1; k < k1; ++k) {
-      const uint16_t key = sp.perm[k];
-      int m = k - 1;
-      while (m >= k0 && sp.perm[m] > key) { sp.perm[m + 1] = sp.perm[m]; --m; }
-      sp.perm[m + 1] = key;
+  // phase A splits the CSC entries over `split` threads, >= 8 entries each
+  // (fewer, longer pieces: a column cut in many pieces is summed serially);
+  // thread t takes entries [s_kb[t], s_kb[t+1])
+  {
+    const int split = E / 8 < 1 ? 1 : (E / 8 < NT ? E / 8 : NT);
+    if (t == 0) s_split = split;
+    s_kb[t] = t < split ? int((int64_t(t) * E) / split) : E;
+    if (t == 0) s_kb[NT] = E;
+    __syncthreads();
+  }
+  if (sp.direct) {
+    // global CSC values: rows descending, each row's (distinct) columns in
+    // parallel, cst[] as a decrementing cursor -> rows ascending per column.
+    // Stored thread-interleaved: entry k of thread t's range at
+    // (k - s_kb[t]) * split + t, so phase A's loads are coalesced.
+    const int split = s_split;
+    for (int r = rows - 1; r >= 0; --r) {
+      for (int e = sp.rp[r] + t; e < sp.rp[r + 1]; e += NT) {
+        const int k = --sp.cst[sp.col[e] - ulo];
+        int o = int((int64_t(k) * split) / E);
+        while (o + 1 < split && s_kb[o + 1] <= k) ++o;
+        while (s_kb[o] > k) --o;
+        const int addr = (k - s_kb[o]) * split + o;
+        sp.cval[addr] = sp.val[e];
+        sp.crow[addr] = uint16_t(r);
+      }
+      __syncthreads();
+    }
+    if (t == 0) sp.cst[W] = E;                      // cst[d] = start of column d
+    __syncthreads();
+  } else {
+    // place entries (slot order within a column is arbitrary here), ...
+    for (int e = t; e < E; e += NT) sp.perm[atomicSub(&sp.cst[sp.col[e] - ulo], 1) - 1] = uint16_t(e);
+    __syncthreads();
+    if (t == 0) sp.cst[W] = E;                      // cst[d] = start of column d
+    __syncthreads();
+    // ... then sort each column by entry index = by row (CSR is row-major):
+    // the rows-ascending order of the dense phase A, independent of the atomics.
+    for (int d = t; d < W; d += NT) {
+      const int k0 = sp.cst[d], k1 = sp.cst[d + 1];
+      for (int k = k0 + 1; k < k1; ++k) {
+        const uint16_t key = sp.perm[k];
+        int m = k - 1;
+        while (m >= k0 && sp.perm[m] > key) { sp.perm[m + 1] = sp.perm[m]; --m; }
+        sp.perm[m + 1] = key;
+      }
     }
   }
   // Compact the nonempty columns in place of cst: cptr[m] (u16 start of the
@@ -503,13 +568,8 @@ __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* 
   if (t == NT - 1) s_nzc = m;                       // last thread holds the total
   __syncthreads();
   if (t == 0) cptr[s_nzc] = uint16_t(E);
-  // phase A splits the CSC entries over `split` threads, >= 8 entries each
-  // (fewer, longer pieces: a column cut in many pieces is summed serially)
-  const int split = E / 8 < 1 ? 1 : (E / 8 < NT ? E / 8 : NT);
-  if (t == 0) s_split = split;
-  __syncthreads();
-  s_kb[t] = t < split ? int((int64_t(t) * E) / split) : E;
-  if (t == 0) s_kb[NT] = E;
+  // thread t's first CSC entry (s_kb) -> its first column (s_m0)
+  const int split = s_split;
   if (t < split) {
     const int kb = int((int64_t(t) * E) / split);
     int lo = 0, hi = s_nzc;                         // cptr[lo] <= kb < cptr[lo + 1]
@@ -528,8 +588,8 @@ __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* 
 // column by column (rows ascending); a column cut by thread boundaries is the
 // left-to-right sum of its pieces, finished by the thread holding its start.
 // Deterministic: the split depends only on the entry count.
-__device__ void phase_a_sparse(int64_t r0, int64_t r1, double* wrow, Smem& sh) {
-  const SparseView sp = sparse_view();
+__device__ void phase_a_sparse(void* sg, int64_t r0, int64_t r1, double* wrow, Smem& sh) {
+  const SparseView sp = sparse_view(sg);
   const int t = threadIdx.x, rows = int(r1 - r0);
   const uint16_t* cptr = reinterpret_cast<const uint16_t*>(sp.cst);
   const uint16_t* ccol = cptr + (kSparseCols + 2);
@@ -542,36 +602,50 @@ __device__ void phase_a_sparse(int64_t r0, int64_t r1, double* wrow, Smem& sh) {
   double tail = 0.0;
   int tail_m = -1;
   if (kb < ke) {
-    const int lo = s_m0[t];
-    int m = lo, mend = cptr[m + 1];
+    // entries are loaded 8 at a time regardless of column boundaries (columns
+    // are short: a load per column would expose the full L2 / shared-memory
+    // latency), then consumed in order with the column bookkeeping in registers
+    int m = s_m0[t], mend = cptr[m + 1];
     bool begun = cptr[m] < kb;                      // column started in an earlier thread
     double acc = 0.0;
-    int k = kb;
-    while (true) {
-      const int stop = mend < ke ? mend : ke;
-      for (; k + 4 <= stop; k += 4) {
-        int e[4];
-        double pv[4], xv[4];
+    const int S = s_split;
+    for (int k0 = kb; k0 < ke; k0 += 8) {
+      double pv[8], xv[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) e[u] = sp.perm[k + u];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) { pv[u] = sp.val[e[u]]; xv[u] = xs[sp.row[e[u]]]; }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc = fma(pv[u], xv[u], acc);
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + u;
+        pv[u] = 0.0;
+        xv[u] = 0.0;
+        if (k < ke) {
+          if (sp.direct) {
+            const int ad = (k - kb) * S + t;
+            pv[u] = sp.cval[ad];
+            xv[u] = xs[sp.crow[ad]];
+          } else {
+            const int e = sp.perm[k];
+            pv[u] = sp.val[e];
+            xv[u] = xs[sp.row[e]];
+          }
+        }
       }
-      for (; k < stop; ++k) {
-        const int e = sp.perm[k];
-        acc = fma(sp.val[e], xs[sp.row[e]], acc);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + u;
+        if (k >= ke) break;
+        if (k == mend) {                            // column m ended inside this thread
+          if (begun) head[t] = acc;
+          else wrow[ulo + ccol[m]] = acc;
+          begun = false;
+          acc = 0.0;
+          ++m;
+          mend = cptr[m + 1];
+        }
+        acc = fma(pv[u], xv[u], acc);
       }
-      if (begun) head[t] = acc;                     // piece of a column begun earlier
-      else if (mend <= ke) wrow[ulo + ccol[m]] = acc;   // whole column inside this thread
-      else { tail = acc; tail_m = m; }              // column continues in later threads
-      if (mend >= ke) break;
-      ++m;
-      mend = cptr[m + 1];
-      begun = false;
-      acc = 0.0;
     }
+    if (begun) head[t] = acc;                       // piece of a column begun earlier
+    else if (mend <= ke) wrow[ulo + ccol[m]] = acc; // whole column inside this thread
+    else { tail = acc; tail_m = m; }                // column continues in later threads
   }
   __syncthreads();
   if (tail_m >= 0) {
@@ -585,8 +659,9 @@ __device__ void phase_a_sparse(int64_t r0, int64_t r1, double* wrow, Smem& sh) {
 // Phase B (sparse): s_i = sum_j P_ij w_j.  The CTA's window of w is staged in
 // shared memory first (one coalesced read); then warp per row, lanes strided
 // over the row's entries, a fixed-tree warp sum.
-__device__ void phase_b_sparse(const double* w, int64_t r0, int64_t r1, double* sv) {   // sv: sh.sv
-  const SparseView sp = sparse_view();
+__device__ void phase_b_sparse(void* sg, const double* w, int64_t r0, int64_t r1,
+                               double* sv) {   // sv: sh.sv
+  const SparseView sp = sparse_view(sg);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, rows = int(r1 - r0);
   const int ulo = s_win_lo[0], W = s_win_hi[0] - ulo;
   double* ws = sp.xs - ulo;                         // ws[j] for window columns j
@@ -597,6 +672,13 @@ __device__ void phase_b_sparse(const double* w, int64_t r0, int64_t r1, double* 
     double dot = 0.0;
     const int e1 = sp.rp[r + 1];
     int e = sp.rp[r] + lane;
+    for (; e + 224 < e1; e += 256) {                // eight loads in flight (global mode)
+      double pv[8], wv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { pv[u] = sp.val[e + 32 * u]; wv[u] = ws[sp.col[e + 32 * u]]; }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dot = fma(pv[u], wv[u], dot);
+    }
     for (; e + 96 < e1; e += 128) {
       double pv[4], wv[4];
 #pragma unroll
@@ -615,8 +697,8 @@ __device__ void phase_b_sparse(const double* w, int64_t r0, int64_t r1, double* 
 // Input: sh.xs[row - r0] (filled by the caller, followed by a barrier).
 __device__ __noinline__ void phase_a(const PlanView v, int64_t r0, int64_t r1, double* wrow,
                                      Smem& sh) {
-  if (v.mode == kPlanSparse) {
-    phase_a_sparse(r0, r1, wrow, sh);
+  if (v.mode >= kPlanSparse) {
+    phase_a_sparse(v.sg, r0, r1, wrow, sh);
     return;
   }
   const int t = threadIdx.x;
@@ -807,8 +889,8 @@ __device__ __forceinline__ void phase_b_ring(const PlanView& v, const double* fi
 // Output: sh.sv[row - r0] (complete after the closing barrier).
 __device__ __noinline__ void phase_b(const PlanView v, const double* w, int64_t r0, int64_t r1,
                                      Smem& sh) {
-  if (v.mode == kPlanSparse) {
-    phase_b_sparse(w, r0, r1, sh.sv);
+  if (v.mode >= kPlanSparse) {
+    phase_b_sparse(v.sg, w, r0, r1, sh.sv);
     return;
   }
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -982,7 +1064,7 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
   const double rPi = row.own && a.rP ? __ldg(a.rP + row.i) : 0.0;
   __syncthreads();
   stage_layout(a, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld);
-  if (s_mode == kPlanSparse) stage_sparse(a, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
+  if (s_mode >= kPlanSparse) stage_sparse(a, r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
 
   if (a.pre_flags) {
     // [0]: plan overflow (materialize), [1]: nonpositive sums (system prep);
@@ -1150,7 +1232,7 @@ __device__ T block_sum_part(T v, T* buf) {                // all threads get the
 
 __global__ void __launch_bounds__(kPartThreads) k_partition(const uint64_t* mask, int64_t n,
                                                             int64_t ld, int64_t mw, int G,
-                                                            int* part) {
+                                                            int sg_ok, int* part) {
   __shared__ int s_pref[kPartRows + 1];      // inclusive prefix of the sparse row costs
   __shared__ int64_t s_buf[32];
   __shared__ int s_ibuf[32];
@@ -1166,7 +1248,11 @@ __global__ void __launch_bounds__(kPartThreads) k_partition(const uint64_t* mask
     sp = block_sum_part<int64_t>(sp, s_buf);
     nz = block_sum_part<int64_t>(nz, s_buf);
     mode = sp * 8 <= kL2ModeBytes ? kPlanL2 : kPlanRing;
-    sparse = ld <= kSparseCols && n <= kPartRows && nz * 5 <= int64_t(G) * kSparseCap * 4;
+    const int64_t cap = sg_ok ? kSparseGCap : kSparseCap;
+    // compressed rows pay 10 B per nonzero per pass (value + column) against
+    // 8 B per span column: only below half density
+    sparse = ld <= kSparseCols && n <= kPartRows && nz * 5 <= int64_t(G) * cap * 4 &&
+             nz * 2 <= n * ld;
   }
   if (sparse) {
     // inclusive prefix of cost_i over rows: 4 contiguous rows per thread
@@ -1206,17 +1292,21 @@ __global__ void __launch_bounds__(kPartThreads) k_partition(const uint64_t* mask
     const int last = int(int64_t(s_pref[n - 1]) * G / total);
     for (int k = last + 1 + t; k <= G; k += kPartThreads) part[k] = int(n);
     __syncthreads();
-    int bad = 0;
+    int bad_smem = 0, bad_glob = 0;
     for (int b = t; b < G; b += kPartThreads) {
       const int r0 = part[b], r1 = part[b + 1];
       const int rows = r1 - r0, nnz = s_pref[r1] - s_pref[r0] - 32 * rows;
-      if (rows > kSparseRows || nnz > kSparseCap) bad = 1;
+      if (rows > kSparseRows || nnz > kSparseCap) bad_smem = 1;
+      if (rows > kSparseRows || nnz > kSparseGCap || !sg_ok) bad_glob = 1;
     }
-    sparse = block_sum_part<int>(bad, s_ibuf) == 0;
+    const int no_smem = block_sum_part<int>(bad_smem, s_ibuf);
+    const int no_glob = block_sum_part<int>(bad_glob, s_ibuf);
+    sparse = no_smem == 0 || no_glob == 0;
+    if (sparse) mode = no_smem == 0 ? kPlanSparse : kPlanSparseG;
   }
   __syncthreads();
   if (sparse) {
-    if (t == 0) part[G + 1] = kPlanSparse;
+    if (t == 0) part[G + 1] = mode;
     return;
   }
   for (int b = t; b <= G; b += kPartThreads) part[b] = int((int64_t(b) * n) / G);
@@ -1229,13 +1319,17 @@ cudaError_t launch_coop(otn_ctx* x, const CoopArgs& a0) {
   CoopArgs a = a0;
   a.stages = kRingDepth;
   a.part = x->part;
-  k_partition<<<1, kPartThreads, 0, x->stream>>>(a.mask, a.n, a.ld, a.mw, x->coop_blocks, x->part);
+  a.sg = x->sg;
+  k_partition<<<1, kPartThreads, 0, x->stream>>>(a.mask, a.n, a.ld, a.mw, x->coop_blocks,
+                                                 x->sg != nullptr, x->part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
   return cudaLaunchCooperativeKernel((void*)k_coop, dim3(x->coop_blocks), dim3(NT), args,
                                      kDynBytes, x->stream);
 }
+
+size_t sparse_g_bytes_per_cta() { return kSparseGBytes; }
 
 int coop_occupancy(int* blocks_per_sm) {
   cudaError_t e = cudaFuncSetAttribute(k_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -49,6 +49,7 @@ struct otn_ctx {
   double* scal;           // 64 device scalars
   int* flags;             // 16 device flag words
   int* part;              // coop_blocks + 2 ints: row partition + plan mode (k_partition)
+  void* sg;               // coop_blocks x kSparseGBytes (ld <= 4096 only; else nullptr)
   otn::DevResult* dres;
   // pinned host mirrors
   double* h_scal;
@@ -95,11 +96,13 @@ struct CoopArgs {
   int stages;             // shared-memory ring stages (set by launch_coop)
   int pad2;
   const int* part;        // row partition + plan mode (k_partition, set by launch_coop)
+  void* sg;               // compressed-rows buffer of kPlanSparseG (nullable; set by launch_coop)
   // workspace
   double *r, *z, *p, *q, *M, *wc, *sv, *wpart, *red;
   DevResult* res;
 };
 cudaError_t launch_coop(otn_ctx* x, const CoopArgs& a);
+size_t sparse_g_bytes_per_cta();        // kPlanSparseG buffer slice (allocated when ld <= 4096)
 
 // Vector kernels and single-CTA reductions.
 cudaError_t launch_vec(otn_ctx* x, int op, int64_t n, double s0, const double* a, const double* b,

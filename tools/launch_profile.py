@@ -41,7 +41,7 @@ tot = sum(r[4] for r in rows)
 print(f"{'mode':>4} {'maxrows':>7} {'nnz':>9} {'hvps':>5} {'us':>9} {'us/hvp':>7}")
 for r in rows:
     print(f"{r[0]:4d} {r[1]:7d} {r[2]:9d} {r[3]:5d} {r[4]:9.1f} {r[4] / max(r[3], 1):7.2f}")
-for mode in (0, 1, 2):
+for mode in (0, 1, 2, 3):
     sel = [r for r in rows if r[0] == mode]
     if sel:
         h = sum(r[3] for r in sel)
