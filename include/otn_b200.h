@@ -123,6 +123,11 @@ int otn_info(const otn_ctx* ctx, int64_t* out4);
  * host[G+1] = plan mode (0 streamed ring, 1 L2-resident direct, 2 sparse
  * shared-memory rows); G = otn_info()[2].  Diagnostic (bench / tests).     */
 int otn_coop_layout(otn_ctx* ctx, int* host);
+/* Stream-ordered copies of n doubles (no host synchronization): device to
+ * device, and host (page-locked for asynchrony) to device.  The solver's
+ * vector bookkeeping (log-marginal caches, targets) on the ctx stream.     */
+int otn_copy(otn_ctx* ctx, double* dst, const double* src, int64_t n);
+int otn_upload(otn_ctx* ctx, double* dst, const double* host_src, int64_t n);
 /* Synchronize and copy the four device status flags to the host:
  * [0] plan overflow, [1] nonpositive sums, [2] reduce domain, [3] rounding. */
 int otn_read_flags(otn_ctx* ctx, int* host4);

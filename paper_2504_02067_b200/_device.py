@@ -145,6 +145,28 @@ class Context:
             self.upload(buf, init)
         return buf
 
+    def upload_async(self, buf, values, slot):
+        """H2D copy of a host vector through a reusable page-locked staging
+        buffer (per `slot`) as one stream-ordered C-ABI copy: no host stall.
+        The staging buffer is reused only after its previous copy completed."""
+        t = torch()
+        pool = self.__dict__.setdefault("_staging", {})
+        ent = pool.get(slot)
+        if ent is None:
+            ent = (t.empty(self.n, dtype=t.float64, pin_memory=True), t.cuda.Event())
+            pool[slot] = ent
+        host, ev = ent
+        ev.synchronize()
+        host.numpy()[:] = np.asarray(values, dtype=np.float64)
+        self.call("otn_upload", vptr(buf), ctypes.c_void_p(host.data_ptr()), self.n)
+        ev.record(t.cuda.current_stream(self.device))
+        TELEMETRY.h2d += host.numel() * 8
+        return buf
+
+    def copy(self, dst, src):
+        """dst[:ld] = src[:ld] on the ctx stream (one C-ABI call)."""
+        self.call("otn_copy", vptr(dst), vptr(src), self.ld)
+
     def upload(self, buf, values):
         t = torch()
         if is_tensor(values):

@@ -73,6 +73,8 @@ SIGNATURES = {
     "otn_set_stream": [_P, _P],
     "otn_info": [_P, ctypes.POINTER(_I64)],
     "otn_read_flags": [_P, _IP],
+    "otn_copy": [_P, _P, _P, _I64],
+    "otn_upload": [_P, _P, _P, _I64],
     "otn_lse_rows": [_P, _P, _D, _P, _P, _P],
     "otn_lse_cols": [_P, _P, _I, _D, _P, _P, _P],
     "otn_rebalance_cols": [_P, _P, _I, _D, _P, _P, _P],

@@ -214,6 +214,20 @@ int otn_info(const otn_ctx* x, int64_t* out4) {
   return OTN_OK;
 }
 
+int otn_copy(otn_ctx* x, double* dst, const double* src, int64_t n) {
+  OTN_REQUIRE(x && dst && src && n >= 0, "otn_copy: bad argument");
+  OTN_CUDA(cudaMemcpyAsync(dst, src, size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice,
+                           x->stream), "otn_copy");
+  return OTN_OK;
+}
+
+int otn_upload(otn_ctx* x, double* dst, const double* host_src, int64_t n) {
+  OTN_REQUIRE(x && dst && host_src && n >= 0, "otn_upload: bad argument");
+  OTN_CUDA(cudaMemcpyAsync(dst, host_src, size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
+                           x->stream), "otn_upload");
+  return OTN_OK;
+}
+
 int otn_coop_layout(otn_ctx* x, int* host) {
   OTN_REQUIRE(x && host, "otn_coop_layout: NULL argument");
   return sync_copy(x, host, x->part, size_t(x->coop_blocks + 2) * sizeof(int), "otn_coop_layout");

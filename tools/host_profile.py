@@ -25,4 +25,4 @@ ot.mdot(dp, 2.0 ** 5, 2.0 ** 16)
 torch.cuda.synchronize()
 pr.disable()
 st = pstats.Stats(pr)
-st.sort_stats("tottime").print_stats(45)
+st.sort_stats(os.environ.get("SORT", "tottime")).print_stats(int(os.environ.get("TOP", "45")))
