@@ -43,39 +43,49 @@ __device__ __forceinline__ double finish(const LseArgs& a, int64_t j, double lse
 // per step, keeps an online (max, sum-exp) pair and rescales at most once per
 // step, so the cost is ~1.1 exp per entry.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kRowThreads) k_lse_rows(LseArgs a) {
+// 4 rows (warps) per 128-thread block: 1024 blocks keep the SMs evenly loaded,
+// and the block stages each 256-column step of the inner vector (with its
+// alpha * dir term, formed once per block instead of once per row) in shared
+// memory, double-buffered with one barrier per step.
+constexpr int kLseRowThreads = 128;
+
+__global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
   __shared__ double2 s_exp[64];
+  __shared__ double s_in[2][256];
   exp_tab_load(s_exp);
-  __syncthreads();
-  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t row = int64_t(blockIdx.x) * (kLseRowThreads / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= a.n) return;
-  const double* crow = a.C + row * a.ld;
+  const bool valid = row < a.n;
+  const double* crow = a.C + (valid ? row : 0) * a.ld;
   const int64_t n = a.n;
   double m = OTN_NINF, s = 0.0;
   // the next step's four 16-byte C loads are issued before this step's math
-  // (the inner vector is L1-resident and loaded in place); j + 1 < ld always
   double2 cur[4], nxt[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int64_t j = 64 * k + 2 * lane;
-    cur[k] = j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
+    cur[k] = valid && j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
   }
+  int buf = 0;
   for (int64_t base = 0; base < n; base += 256) {
+    for (int jj = threadIdx.x; jj < 256; jj += kLseRowThreads) {
+      const int64_t j = base + jj;
+      s_in[buf][jj] = j < n ? eff(a.inner, a.inner_d, a.alpha, j) : 0.0;
+    }
+    __syncthreads();                                 // also publishes s_exp on the first step
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t j = base + 256 + 64 * k + 2 * lane;
-      nxt[k] = j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
+      nxt[k] = valid && j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
     }
     double b[8];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int64_t j = base + 64 * k + 2 * lane;
-      b[2 * k] = j < n ? __dadd_rn(__dmul_rn(a.ng, cur[k].x), eff(a.inner, a.inner_d, a.alpha, j))
-                       : OTN_NINF;
-      b[2 * k + 1] = j + 1 < n
-          ? __dadd_rn(__dmul_rn(a.ng, cur[k].y), eff(a.inner, a.inner_d, a.alpha, j + 1))
-          : OTN_NINF;
+      const int jl = 64 * k + 2 * lane;
+      const int64_t j = base + jl;
+      const double2 in = *reinterpret_cast<const double2*>(&s_in[buf][jl]);
+      b[2 * k] = j < n ? __dadd_rn(__dmul_rn(a.ng, cur[k].x), in.x) : OTN_NINF;
+      b[2 * k + 1] = j + 1 < n ? __dadd_rn(__dmul_rn(a.ng, cur[k].y), in.y) : OTN_NINF;
     }
     double cm = b[0];
 #pragma unroll
@@ -90,9 +100,10 @@ __global__ void __launch_bounds__(kRowThreads) k_lse_rows(LseArgs a) {
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) cur[k] = nxt[k];
+    buf ^= 1;
   }
   warp_lse(m, s);
-  if (lane == 0) a.out[row] = finish(a, row, lse_value(m, s));
+  if (valid && lane == 0) a.out[row] = finish(a, row, lse_value(m, s));
 }
 
 // ---------------------------------------------------------------------------
@@ -322,7 +333,7 @@ cudaError_t launch_lse_rows(otn_ctx* x, const double* C, double ng, const double
                             const double* outer_d, const double* inner, const double* inner_d,
                             double alpha, int mode, double* out) {
   LseArgs a{C, x->n, x->ld, ng, outer, outer_d, inner, inner_d, alpha, mode, out};
-  k_lse_rows<<<rows_grid(x->n, kRowThreads), kRowThreads, 0, x->stream>>>(a);
+  k_lse_rows<<<rows_grid(x->n, kLseRowThreads), kLseRowThreads, 0, x->stream>>>(a);
   return cudaGetLastError();
 }
 
