@@ -141,7 +141,7 @@ struct PlanView {
   int64_t ld, mw;
   int nt;                   // tiles
   int mode;                 // PlanMode
-  uint32_t* span;           // staged spans: lo | hi << 16, relative to the tile
+  uint32_t span_off;        // byte offset of the staged spans (lo | hi << 16) in s_ring
   void* sg;                 // kPlanSparseG buffer
 };
 
@@ -167,11 +167,16 @@ constexpr size_t kSparsePerm = kSparseRow + size_t(kSparseCap) * 2;     // u16[c
 constexpr size_t kSparseBytes = kSparsePerm + size_t(kSparseCap) * 2;
 
 // The (row, tile) spans live in the dynamic region after what the mode uses.
-__device__ __forceinline__ uint32_t* span_base(int mode) {
-  char* b = reinterpret_cast<char*>(s_ring);
-  return reinterpret_cast<uint32_t*>(b + (mode == kPlanRing ? kRingBytes
-                                          : mode == kPlanSparse ? kSparseBytes
-                                          : mode == kPlanSparseG ? kSparseVal : 0));
+__device__ __forceinline__ uint32_t span_offset(int mode) {
+  return uint32_t(mode == kPlanRing ? kRingBytes
+                  : mode == kPlanSparse ? kSparseBytes
+                  : mode == kPlanSparseG ? kSparseVal : 0);
+}
+
+// Spans are indexed off the extern __shared__ array itself so the compiler
+// emits shared-memory loads (a pointer carried in a struct would be generic).
+__device__ __forceinline__ uint32_t* span_ptr(uint32_t off) {
+  return reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(s_ring) + off);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -201,7 +206,7 @@ __device__ __forceinline__ void mask_span(const PlanView& v, int64_t i, int ti, 
 
 // Span of row r0 + il (il = row index within the CTA) in tile ti.
 __device__ __forceinline__ void get_span(const PlanView& v, int il, int ti, int& lo, int& hi) {
-  const uint32_t s = v.span[il * v.nt + ti];
+  const uint32_t s = span_ptr(v.span_off)[il * v.nt + ti];
   lo = int(s & 0xffffu);
   hi = int(s >> 16);
 }
@@ -220,7 +225,7 @@ __device__ PlanView plan_view(const CoopArgs& a, int64_t r0, int64_t r1) {
   v.mw = a.mw;
   v.nt = ntiles_of(a.ld);
   v.mode = s_mode;
-  v.span = span_base(v.mode);
+  v.span_off = span_offset(v.mode);
   v.sg = a.sg;
   return v;
 }
@@ -237,7 +242,7 @@ __device__ void stage_layout(const CoopArgs& a, int64_t r0, int64_t r1, double* 
     const int ti = int(k % v.nt);
     int lo, hi;
     mask_span(v, r0 + k / v.nt, ti, lo, hi);
-    v.span[k] = uint32_t(lo) | (uint32_t(hi) << 16);
+    span_ptr(v.span_off)[k] = uint32_t(lo) | (uint32_t(hi) << 16);
     if (lo < hi) {
       atomicMin(&s_win_lo[ti], lo);
       atomicMax(&s_win_hi[ti], hi);
