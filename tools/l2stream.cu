@@ -127,6 +127,48 @@ __global__ void __launch_bounds__(NT, 1) k_bulk(const double* P, int span, int r
   out[blockIdx.x * NT + t] = acc.x + acc.y;
 }
 
+
+// K4: bulk-copy ring with full/empty mbarriers (producer = thread 0; each of
+// the 16 consumer warps releases a slot after reading it).
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+template <int D>
+__global__ void __launch_bounds__(NT, 1) k_bulk2(const double* P, int span, int rows, int reps, double* out) {
+  __shared__ __align__(8) unsigned long long full[D], empty[D];
+  const int t = threadIdx.x, lane = t & 31;
+  const double* base = P + size_t(blockIdx.x) * rows * LD + 1024;
+  const unsigned ring0 = unsigned(__cvta_generic_to_shared(ring));
+  const unsigned slot = unsigned(span) * 8u;
+  if (t < D) {
+    mbar_init(unsigned(__cvta_generic_to_shared(&full[t])), 1);
+    mbar_init(unsigned(__cvta_generic_to_shared(&empty[t])), NT / 32);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int total = reps * rows;
+  int issued = 0;
+  auto issue = [&](int k) {
+    const int s = k % D;
+    if (k >= D) mbar_wait(unsigned(__cvta_generic_to_shared(&empty[s])), ((k / D) - 1) & 1);
+    const unsigned bar = unsigned(__cvta_generic_to_shared(&full[s]));
+    mbar_expect(bar, slot);
+    bulk_g2s(ring0 + s * slot, base + size_t(k % rows) * LD, slot, bar);
+  };
+  if (t == 0) for (; issued < D - 1 && issued < total; ++issued) issue(issued);
+  double2 acc = make_double2(0, 0);
+  for (int c = 0; c < total; ++c) {
+    if (t == 0 && issued < total) { issue(issued); ++issued; }
+    const int s = c % D;
+    mbar_wait(unsigned(__cvta_generic_to_shared(&full[s])), (c / D) & 1);
+    const double2* row = ring + s * (span / 2);
+    for (int j = t; j < span / 2; j += NT) { const double2 v = row[j]; acc.x += v.x; acc.y += v.y; }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(unsigned(__cvta_generic_to_shared(&empty[s])));
+  }
+  out[blockIdx.x * NT + t] = acc.x + acc.y;
+}
+
 template <typename F>
 float timeit(F f) {
   cudaEvent_t a, b;
@@ -167,6 +209,12 @@ int main(int argc, char** argv) {
     cudaFuncSetAttribute(k_bulk<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);        \
     rep("bulk D=" #D, timeit([&] { k_bulk<D><<<G, NT, smem>>>(P, span, rows, reps, out); }));  \
   }
-  BULK(2) BULK(4) BULK(8) BULK(16) BULK(24)
+  BULK(4) BULK(16)
+#define BULK2(D)                                                                                \
+  if (D * span * 8 <= smem) {                                                                   \
+    cudaFuncSetAttribute(k_bulk2<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);       \
+    rep("bulk2 D=" #D, timeit([&] { k_bulk2<D><<<G, NT, smem>>>(P, span, rows, reps, out); })); \
+  }
+  BULK2(2) BULK2(4) BULK2(6) BULK2(8) BULK2(16) BULK2(24)
   return 0;
 }
