@@ -743,7 +743,11 @@ __device__ __noinline__ void phase_a(const PlanView v, int64_t r0, int64_t r1, d
 //   kind 0: out = w / cP     (the HVP's inner vector, and apply_pc)
 //   kind 1: out = -(w / cP)  (d_v, projector.py:201)
 //   kind 2: out = w          (rmatvec)
-__device__ __noinline__ void phase_a2(const CoopArgs& a, int kind, double* out, Smem& sh) {
+//   wprev / wkeep (CG pipelining, pcg below): w = sum_b wpart[b] + beta * wprev
+//   before the kind is applied, and w is kept in wkeep (may alias wprev).
+__device__ __noinline__ void phase_a2(const CoopArgs& a, int kind, double* out, Smem& sh,
+                                      const double* wprev = nullptr, double beta = 0.0,
+                                      double* wkeep = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = gridDim.x;
   for (int64_t s = blockIdx.x; s * 32 < a.ld; s += G) {
@@ -766,6 +770,8 @@ __device__ __noinline__ void phase_a2(const CoopArgs& a, int kind, double* out, 
       double tot = 0.0;
 #pragma unroll 8
       for (int w = 0; w < NW; ++w) tot += sh.a2[w][lane];
+      if (wprev) tot = __dadd_rn(tot, __dmul_rn(beta, __ldcg(wprev + j)));
+      if (wkeep) wkeep[j] = tot;
       double val = 0.0;
       if (j < a.n) {
         val = kind == 2 ? tot : __ddiv_rn(tot, __ldg(a.cP + j));
@@ -986,11 +992,19 @@ struct PcgOut {
 
 // Jacobi-PCG, newton.py:123-172, on register rows.  b == nullptr means b = -g.
 // x: in (if has_x0) / out.
-__device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, double rPi,
-                      double rho, const double* bvec, double tol, double& x, bool has_x0,
-                      int64_t max_iters, int64_t r0, int64_t r1, int& slot, Smem& sh,
-                      int64_t& nh) {
+//
+// Pipelined matvec: the phase-A partials of the next direction are formed
+// from z BEFORE the r.z reduction, and phase A2 combines them as
+// P^T p_new = P^T z + beta * P^T p (the previous direction's column sums are
+// kept in a.q), so the r.z barrier doubles as the HVP's partials barrier:
+// 3 grid barriers per CG iteration instead of 4.  The CG recurrences (x, r,
+// z, p, alpha, beta and the stopping tests) are the reference's, operation
+// for operation; only the column sums of P^T p are formed by linearity.
+__device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, double rPi, double rho,
+                      const double* bvec, double tol, double& x, bool has_x0, int64_t max_iters,
+                      int64_t r0, int64_t r1, int& slot, Smem& sh, int64_t& nh) {
   PcgOut o{OTN_OK, 0, 0.0};
+  const bool mv = rho != 0.0;                       // F(0) = diag(rP): no plan passes
   double q = 0.0;
   if (has_x0) q = hvp(grid, a, x, rho, rPi, r0, r1, sh, nh);
   double M = 1.0, bi = 0.0, r = 0.0, z = 0.0, p = 0.0;
@@ -1012,13 +1026,28 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
   } else {
     x = 0.0;
   }
+  double* wrow = a.wpart + int64_t(blockIdx.x) * a.ld;
+  if (mv) {                                         // partials of the first direction p = z
+    stage_x(p, sh);
+    phase_a(plan_view(a, r0, r1), r0, r1, wrow, sh);
+  }
   grid_reduce<3>(grid, loc, a.red, slot, sh);
   if (loc[2] > 0.0) { o.status = OTN_ST_PRECOND; return o; }
   if (loc[0] <= tol) { o.resid = loc[0]; return o; }
   double rz = loc[1];
   double norm = loc[0];
+  double beta = 0.0;
+  bool fresh = true;                                // no previous direction yet
   for (int64_t k = 1; k <= max_iters; ++k) {
-    q = hvp(grid, a, p, rho, rPi, r0, r1, sh, nh);
+    q = __dmul_rn(rPi, p);
+    if (mv) {
+      ++nh;
+      phase_a2(a, 0, a.wc, sh, fresh ? nullptr : a.q, beta, a.q);
+      grid.sync();
+      phase_b(plan_view(a, r0, r1), a.wc, r0, r1, sh);   // ends with a barrier
+      q = row.own ? __dsub_rn(q, __dmul_rn(rho, sh.sv[threadIdx.x])) : 0.0;
+    }
+    fresh = false;
     double pq[1] = {fma(p, q, 0.0)};
     grid_reduce<1>(grid, pq, a.red, slot, sh);
     if (pq[0] <= 0.0) { o.status = OTN_ST_BREAKDOWN; o.iters = k; o.resid = pq[0]; return o; }
@@ -1031,11 +1060,15 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
     }
     if (!row.own) r = 0.0;
     z = __ddiv_rn(r, M);
+    if (mv) {                                       // partials of z, read after the barrier
+      stage_x(z, sh);
+      phase_a(plan_view(a, r0, r1), r0, r1, wrow, sh);
+    }
     double nz[2] = {fabs(r), fma(r, z, 0.0)};
     grid_reduce<2>(grid, nz, a.red, slot, sh);
     norm = nz[0];
     if (norm <= tol) { o.iters = k; o.resid = norm; return o; }
-    const double beta = nz[1] / rz;
+    beta = nz[1] / rz;
     p = __dadd_rn(z, __dmul_rn(beta, p));
     rz = nz[1];
   }
