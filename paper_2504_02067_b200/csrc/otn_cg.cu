@@ -745,9 +745,13 @@ __device__ __noinline__ void phase_a(const PlanView v, int64_t r0, int64_t r1, d
 //   kind 2: out = w          (rmatvec)
 //   wprev / wkeep (CG pipelining, pcg below): w = sum_b wpart[b] + beta * wprev
 //   before the kind is applied, and w is kept in wkeep (may alias wprev).
-__device__ __noinline__ void phase_a2(const CoopArgs& a, int kind, double* out, Smem& sh,
-                                      const double* wprev = nullptr, double beta = 0.0,
-                                      double* wkeep = nullptr) {
+// Returns this thread's share of sum_j w_j * out_j over its columns (warp 0
+// lanes; 0 elsewhere) -- for kind 0 that is sum_j w_j^2 / cP_j = p^T P (P^T p / cP),
+// the matvec part of p.q (see pcg).
+__device__ __noinline__ double phase_a2(const CoopArgs& a, int kind, double* out, Smem& sh,
+                                        const double* wprev = nullptr, double beta = 0.0,
+                                        double* wkeep = nullptr) {
+  double wq = 0.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = gridDim.x;
   for (int64_t s = blockIdx.x; s * 32 < a.ld; s += G) {
@@ -776,11 +780,13 @@ __device__ __noinline__ void phase_a2(const CoopArgs& a, int kind, double* out, 
       if (j < a.n) {
         val = kind == 2 ? tot : __ddiv_rn(tot, __ldg(a.cP + j));
         if (kind == 1) val = -val;
+        wq = fma(tot, val, wq);
       }
       out[j] = val;
     }
     __syncthreads();
   }
+  return wq;
 }
 
 // Sum eight per-lane values over the warp with a transpose-reduction (fixed
@@ -1039,19 +1045,27 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
   double beta = 0.0;
   bool fresh = true;                                // no previous direction yet
   for (int64_t k = 1; k <= max_iters; ++k) {
+    // p.q = sum_i rP_i p_i^2 - rho * sum_j w_j (w_j / cP_j), w = P^T p: both
+    // sums are known once A2 has run, so their reduction IS the barrier
+    // between A2 and phase B (one barrier fewer than p.q after phase B).
     q = __dmul_rn(rPi, p);
+    double pq;
     if (mv) {
       ++nh;
-      phase_a2(a, 0, a.wc, sh, fresh ? nullptr : a.q, beta, a.q);
-      grid.sync();
+      const double wq = phase_a2(a, 0, a.wc, sh, fresh ? nullptr : a.q, beta, a.q);
+      double sums[2] = {fma(p, q, 0.0), wq};
+      grid_reduce<2>(grid, sums, a.red, slot, sh);
+      pq = __dsub_rn(sums[0], __dmul_rn(rho, sums[1]));
       phase_b(plan_view(a, r0, r1), a.wc, r0, r1, sh);   // ends with a barrier
       q = row.own ? __dsub_rn(q, __dmul_rn(rho, sh.sv[threadIdx.x])) : 0.0;
+    } else {
+      double pq1[1] = {fma(p, q, 0.0)};
+      grid_reduce<1>(grid, pq1, a.red, slot, sh);
+      pq = pq1[0];
     }
     fresh = false;
-    double pq[1] = {fma(p, q, 0.0)};
-    grid_reduce<1>(grid, pq, a.red, slot, sh);
-    if (pq[0] <= 0.0) { o.status = OTN_ST_BREAKDOWN; o.iters = k; o.resid = pq[0]; return o; }
-    const double alpha = rz / pq[0];
+    if (pq <= 0.0) { o.status = OTN_ST_BREAKDOWN; o.iters = k; o.resid = pq; return o; }
+    const double alpha = rz / pq;
     x = __dadd_rn(x, __dmul_rn(alpha, p));
     r = __dsub_rn(r, __dmul_rn(alpha, q));
     if (k % kRefresh == 0) {
