@@ -40,6 +40,7 @@ struct Smem {
   double a2[NW][33];
   double xs[NT];                    // phase A input: x of the CTA's rows (row - r0)
   double sv[NT];                    // phase B output: (P w) of the CTA's rows
+  double2 rbuf[2][kRedStride / 2];  // grid_reduce_begin/end: the G partials, fetched async
   double bp[NW][kRows];             // phase B: per-warp partial row dots
 };
 
@@ -85,6 +86,71 @@ __device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&v)[K]
     double t = 0.0;
 #pragma unroll
     for (int m = 0; m < kRedStride / 64; ++m) t += part[m].x + part[m].y;
+    t = warp_sum(t);
+    if (lane == 0) sh.gres[warp] = t;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = sh.gres[k];
+  slot ^= 1;
+}
+
+// The same reduction split around independent work: grid_reduce_begin does
+// the barrier and starts copying the G partials into shared memory
+// (cp.async, zero-filled past G); grid_reduce_end waits for them and sums in
+// the same fixed order.  Whatever runs in between (phase B of the HVP) hides
+// the partials' load latency.  K <= 2.
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0) : "memory");
+}
+
+template <int K>
+__device__ __forceinline__ void grid_reduce_begin(cg::grid_group& grid, double (&v)[K], double* red,
+                                                  int slot, Smem& sh) {
+  static_assert(K <= 2, "rbuf holds two values");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = gridDim.x;
+  double* base = red + int64_t(slot) * kRedWidth * kRedStride;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) sh.red[k][warp] = v[k];
+  }
+  __syncthreads();
+  if (warp < K) {
+    const double t = warp_sum(lane < NW ? sh.red[warp][lane] : 0.0);
+    if (lane == 0) base[warp * kRedStride + blockIdx.x] = t;
+  }
+  grid.sync();
+  if (warp < K) {
+    const double* src = base + warp * kRedStride;
+#pragma unroll
+    for (int m = 0; m < kRedStride / 64; ++m) {
+      const int b = 64 * m + 2 * lane;
+      cp_async16_zfill(static_cast<uint32_t>(__cvta_generic_to_shared(&sh.rbuf[warp][32 * m + lane])),
+                       src + (b < G ? b : 0), b < G);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void grid_reduce_end(double (&v)[K], int& slot, Smem& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = gridDim.x;
+  if (warp < K) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    double t = 0.0;
+#pragma unroll
+    for (int m = 0; m < kRedStride / 64; ++m) {
+      const int b = 64 * m + 2 * lane;
+      double2 pr = sh.rbuf[warp][32 * m + lane];
+      if (b + 1 == G) pr.y = 0.0;                   // odd G: the pair's second slot is not a CTA
+      t += pr.x + pr.y;
+    }
     t = warp_sum(t);
     if (lane == 0) sh.gres[warp] = t;
   }
@@ -156,7 +222,7 @@ constexpr size_t kRingBytes = size_t(kRingDepth) * CH * NT * 16;
 // kPlanSparse shared-memory layout (dynamic region; see the sparse section).
 constexpr int kSparseRows = 512;                    // rows per CTA
 constexpr int kSparseCols = TILE;                   // one tile (ld <= 4096)
-constexpr int kSparseCap = 10900;                   // nonzeros per CTA (fits 227 KB with the statics)
+constexpr int kSparseCap = 10600;                   // nonzeros per CTA (fits 227 KB with the statics)
 constexpr size_t kSparseXs = 0;                     // double[kSparseCols]: x rows (A) / w window (B)
 constexpr size_t kSparseRp = kSparseXs + kSparseCols * 8;               // int[kSparseRows + 1]
 constexpr size_t kSparseCst = kSparseRp + (kSparseRows + 4) * 4;        // int[kSparseCols + 1]
@@ -789,6 +855,59 @@ __device__ __noinline__ double phase_a2(const CoopArgs& a, int kind, double* out
   return wq;
 }
 
+// Phase A2 split for the CG pipeline (used when every CTA owns at most one
+// 32-column slice, ld <= 32 G): a2_sums loads and sums the partials of the
+// CTA's slice per warp (no scalar needed yet); a2_tail (warp 0) finishes
+// the slice once beta is known.  Same arithmetic as phase_a2.
+__device__ __forceinline__ bool a2_single_slice(const CoopArgs& a) {
+  return a.ld <= int64_t(32) * gridDim.x;
+}
+
+__device__ __noinline__ void a2_sums(const CoopArgs& a, Smem& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = gridDim.x;
+  const int64_t s = blockIdx.x;
+  if (s * 32 >= a.ld) return;
+  const int64_t j = s * 32 + lane;
+  double acc = 0.0;
+  for (int b0 = warp; b0 < G; b0 += NW * 16) {
+    double v[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int bp = b0 + m * NW;
+      v[m] = bp < G ? __ldcg(a.wpart + int64_t(bp) * a.ld + j) : 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < 16; ++m) acc += v[m];
+  }
+  sh.a2[warp][lane] = acc;
+}
+
+// After a2_sums and a barrier: out_j = w_j / cP_j (kind 0) with
+// w = sum + beta * wprev (if wprev), w kept in wkeep; returns w_j * out_j
+// for warp 0's lanes.
+__device__ __forceinline__ double a2_tail(const CoopArgs& a, double* out, Smem& sh,
+                                          const double* wprev, double beta, double* wkeep) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t s = blockIdx.x;
+  double wq = 0.0;
+  if (warp == 0 && s * 32 < a.ld) {
+    const int64_t j = s * 32 + lane;
+    double tot = 0.0;
+#pragma unroll 8
+    for (int w = 0; w < NW; ++w) tot += sh.a2[w][lane];
+    if (wprev) tot = __dadd_rn(tot, __dmul_rn(beta, __ldcg(wprev + j)));
+    if (wkeep) wkeep[j] = tot;
+    double val = 0.0;
+    if (j < a.n) {
+      val = __ddiv_rn(tot, __ldg(a.cP + j));
+      wq = fma(tot, val, wq);
+    }
+    out[j] = val;
+  }
+  return wq;
+}
+
 // Sum eight per-lane values over the warp with a transpose-reduction (fixed
 // butterfly, 9 shuffles instead of 8 x 5): on return lane l holds the total of
 // value ((l>>4)&1)*4 + ((l>>3)&1)*2 + ((l>>2)&1).
@@ -1044,19 +1163,39 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
   double norm = loc[0];
   double beta = 0.0;
   bool fresh = true;                                // no previous direction yet
+  const bool split = mv && a2_single_slice(a);      // overlap the r.z reduction with A2's loads
+  bool pending = false;                             // an r.z reduction begun, not finished
+  double nz[2] = {0.0, 0.0};
   for (int64_t k = 1; k <= max_iters; ++k) {
     // p.q = sum_i rP_i p_i^2 - rho * sum_j w_j (w_j / cP_j), w = P^T p: both
     // sums are known once A2 has run, so their reduction IS the barrier
     // between A2 and phase B (one barrier fewer than p.q after phase B).
+    double wq = 0.0;
+    if (pending) {
+      // finish the previous iteration's r.z reduction under A2's partial loads
+      a2_sums(a, sh);
+      grid_reduce_end<2>(nz, slot, sh);             // its closing barrier publishes sh.a2
+      pending = false;
+      norm = nz[0];
+      if (norm <= tol) { o.iters = k - 1; o.resid = norm; return o; }
+      beta = nz[1] / rz;
+      p = __dadd_rn(z, __dmul_rn(beta, p));
+      rz = nz[1];
+      ++nh;
+      wq = a2_tail(a, a.wc, sh, fresh ? nullptr : a.q, beta, a.q);
+    }
     q = __dmul_rn(rPi, p);
     double pq;
     if (mv) {
-      ++nh;
-      const double wq = phase_a2(a, 0, a.wc, sh, fresh ? nullptr : a.q, beta, a.q);
+      if (!split || fresh) {
+        ++nh;
+        wq = phase_a2(a, 0, a.wc, sh, fresh ? nullptr : a.q, beta, a.q);
+      }
       double sums[2] = {fma(p, q, 0.0), wq};
-      grid_reduce<2>(grid, sums, a.red, slot, sh);
-      pq = __dsub_rn(sums[0], __dmul_rn(rho, sums[1]));
+      grid_reduce_begin<2>(grid, sums, a.red, slot, sh);
       phase_b(plan_view(a, r0, r1), a.wc, r0, r1, sh);   // ends with a barrier
+      grid_reduce_end<2>(sums, slot, sh);
+      pq = __dsub_rn(sums[0], __dmul_rn(rho, sums[1]));
       q = row.own ? __dsub_rn(q, __dmul_rn(rho, sh.sv[threadIdx.x])) : 0.0;
     } else {
       double pq1[1] = {fma(p, q, 0.0)};
@@ -1078,13 +1217,24 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
       stage_x(z, sh);
       phase_a(plan_view(a, r0, r1), r0, r1, wrow, sh);
     }
-    double nz[2] = {fabs(r), fma(r, z, 0.0)};
+    nz[0] = fabs(r);
+    nz[1] = fma(r, z, 0.0);
+    if (split) {
+      grid_reduce_begin<2>(grid, nz, a.red, slot, sh);
+      pending = true;
+      continue;                                     // finished at the top of the next iteration
+    }
     grid_reduce<2>(grid, nz, a.red, slot, sh);
     norm = nz[0];
     if (norm <= tol) { o.iters = k; o.resid = norm; return o; }
     beta = nz[1] / rz;
     p = __dadd_rn(z, __dmul_rn(beta, p));
     rz = nz[1];
+  }
+  if (pending) {                                    // the budget ran out on a begun reduction
+    grid_reduce_end<2>(nz, slot, sh);
+    norm = nz[0];
+    if (norm <= tol) { o.iters = max_iters; o.resid = norm; return o; }
   }
   o.status = OTN_ST_NONCONVERGENCE;
   o.iters = max_iters;
