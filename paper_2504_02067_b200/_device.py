@@ -163,6 +163,26 @@ class Context:
         TELEMETRY.h2d += host.numel() * 8
         return buf
 
+    def upload_rows_async(self, block, rows, slot):
+        """block[i, :n] = rows[i] for a contiguous (k, ld) device block, as ONE
+        stream-ordered copy from page-locked staging (padding copied as 0)."""
+        t = torch()
+        pool = self.__dict__.setdefault("_staging", {})
+        key = (slot, block.shape[0])
+        ent = pool.get(key)
+        if ent is None:
+            ent = (t.zeros(block.shape, dtype=t.float64, pin_memory=True), t.cuda.Event())
+            pool[key] = ent
+        host, ev = ent
+        ev.synchronize()
+        h = host.numpy()
+        for i, v in enumerate(rows):
+            h[i, : self.n] = v
+        self.call("otn_upload", vptr(block), ctypes.c_void_p(host.data_ptr()), block.numel())
+        ev.record(t.cuda.current_stream(self.device))
+        TELEMETRY.h2d += host.numel() * 8
+        return block
+
     def copy(self, dst, src):
         """dst[:ld] = src[:ld] on the ctx stream (one C-ABI call)."""
         self.call("otn_copy", vptr(dst), vptr(src), self.ld)

@@ -121,13 +121,14 @@ class DualState:
         self.r = r
         self.c = c
         k = self._ctx
-        if getattr(self, "_r", None) is None:
-            self._r, self._c, self._log_r, self._log_c = (k.vec() for _ in range(4))
-        k.upload_async(self._r, self.r, "r")
-        k.upload_async(self._c, self.c, "c")
+        if getattr(self, "_tgt", None) is None:
+            t = torch()
+            # r, c, log r, log c as rows of one device block: one H2D copy
+            self._tgt = t.zeros((4, k.ld), dtype=t.float64, device=k.device)
+            self._r, self._c, self._log_r, self._log_c = self._tgt.unbind(0)
         with np.errstate(divide="ignore", invalid="ignore"):
-            k.upload_async(self._log_r, np.log(self.r), "log_r")
-            k.upload_async(self._log_c, np.log(self.c), "log_c")
+            k.upload_rows_async(self._tgt, (self.r, self.c, np.log(self.r), np.log(self.c)),
+                                "targets")
         self._targets_copy = (self.r.copy(), self.c.copy())
         self._rowstat = None
 
