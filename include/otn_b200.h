@@ -120,8 +120,8 @@ int otn_set_stream(otn_ctx* ctx, void* stream);
 int otn_info(const otn_ctx* ctx, int64_t* out4);
 /* Synchronize and copy the row partition and plan mode of the last
  * persistent-solver launch: host[0..G] = row boundaries of the G CTAs,
- * host[G+1] = plan mode (0 streamed ring, 1 L2-resident direct, 2 sparse
- * shared-memory rows); G = otn_info()[2].  Diagnostic (bench / tests).     */
+ * host[G+1] = plan mode (0 streamed ring, 2 sparse shared-memory rows, 3
+ * sparse global-memory rows; 1 is retired); G = otn_info()[2].  Diagnostic (bench / tests).     */
 int otn_coop_layout(otn_ctx* ctx, int* host);
 /* Stream-ordered copies of n doubles (no host synchronization): device to
  * device, and host (page-locked for asynchrony) to device.  The solver's

@@ -161,7 +161,7 @@ __device__ __forceinline__ void grid_reduce_end(double (&v)[K], int& slot, Smem&
 }
 
 // ---------------------------------------------------------------------------
-// Plan streaming: per-CTA column windows + register-staged direct loads.
+// Plan streaming (dense plans): per-CTA column windows + cp.async rings.
 //
 // A work item is one row i of one 4096-column tile T of the plan; its span
 // [lo, hi) runs from the first to the last nonzero 64-column segment
@@ -169,23 +169,22 @@ __device__ __forceinline__ void grid_reduce_end(double (&v)[K], int& slot, Smem&
 // regularization; for pixel-grid costs a row's nonzero segments are one
 // contiguous run).  At kernel start each CTA stages the spans of its rows and
 // their union per tile — its column WINDOW — in shared memory.  Within a tile
-// thread t owns window columns {2t, 2t+1} + c*1024 (c < nch = ceil(W/1024)),
-// so for a sparse plan all threads work on the few nonzero columns instead of
-// most of them idling.  Each thread loads its 16-byte chunks of U rows at once
-// (ld.global.cg, predicated on the span) before using them: the loads of a
-// batch are independent, so a warp keeps U * nch requests in flight with no
-// shared-memory staging and no barrier inside a phase.  (A per-thread
-// cp.async ring was measured 3-5x slower on L2-resident spans:
-// tools/l2stream.cu.)  Chunks outside the span are exact zeros and are neither
-// loaded nor used: the results equal the dense computation bit for bit.
+// thread t owns window columns {2t, 2t+1} + c*1024, so for a sparse-ish plan
+// all threads work on the few nonzero columns instead of most of them idling.
+// Chunks outside the span are exact zeros and are neither loaded nor used:
+// the results equal the dense computation bit for bit.  (Register-batched
+// ld.global.cg was the faster path for L2-resident spans in isolation,
+// tools/l2stream.cu, but lost to the ring inside the kernel once the sparse
+// modes below took the late stages; it was retired.)
 // ---------------------------------------------------------------------------
 constexpr int kSpanSmem = 8192;                     // (row, tile) spans staged per CTA (32 KB)
 constexpr int kMaxTiles = 64;                       // ld <= 262144
 __shared__ int s_win_lo[kMaxTiles], s_win_hi[kMaxTiles];
 // Plan mode of this launch (chosen by k_partition, uniform over the grid):
 //   kPlanRing    plan streamed from HBM through per-thread cp.async rings;
-//   kPlanL2      the masked plan (sum of row spans) fits in L2: register-
-//                batched direct loads;
+//   kPlanL2      (retired: register-batched direct loads of L2-resident
+//                spans; measured no faster than the ring once the sparse
+//                modes took the late stages, and its code cost I-cache)
 //   kPlanSparse  each CTA compresses its rows' nonzeros into shared memory
 //                once per launch (CSR for P w, a local CSC for P^T x);
 //   kPlanSparseG the same compressed rows in a per-CTA slice of global memory
@@ -197,7 +196,6 @@ __shared__ int s_nzc;                               // kPlanSparse: nonempty col
 __shared__ int s_split;                             // kPlanSparse: threads splitting the CSC entries
 __shared__ uint16_t s_m0[kCoopThreads];             // kPlanSparse: column of each thread's first entry
 __shared__ int s_kb[kCoopThreads + 1];              // kPlanSparse: first CSC entry of each thread
-constexpr int64_t kL2ModeBytes = 80ll * 1024 * 1024;
 
 // Everything the streaming loops need, by value (registers, not the kernel's
 // parameter copy in local memory).
@@ -325,44 +323,6 @@ __device__ void stage_layout(const CoopArgs& a, int64_t r0, int64_t r1, double* 
   __syncthreads();
 }
 
-// Load this thread's chunks of one row (zeros outside the span).
-template <int NCH>
-__device__ __forceinline__ void load_row(const double* row, int lo, int hi, int col0,
-                                         double2 (&pv)[NCH]) {
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    const int col = col0 + c * NT * 2;
-    pv[c] = in_span(col, lo, hi) ? ldcg2(row + col) : make_double2(0.0, 0.0);
-  }
-}
-
-// Phase A over one tile, rows [c0, c0 + m) of the CTA: acc[c] += P_ij x_i
-// (rows ascending; a zero chunk leaves acc unchanged bit for bit).
-template <int NCH>
-__device__ __forceinline__ void phase_a_tile(const PlanView& v, const double* row0, int c0, int m,
-                                             int ti, int col0, double2 (&acc)[CH], const Smem& sh) {
-  constexpr int U = NCH <= 2 ? 8 : 4;
-  for (int q0 = 0; q0 < m; q0 += U) {
-    double2 pv[U][NCH];
-    double xi[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      int lo = 0, hi = 0;
-      if (q0 + u < m) get_span(v, c0 + q0 + u, ti, lo, hi);
-      xi[u] = sh.xs[c0 + (q0 + u < m ? q0 + u : 0)];
-      load_row<NCH>(row0 + int64_t(q0 + u) * v.ld, lo, hi, col0, pv[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        acc[c].x = fma(pv[u][c].x, xi[u], acc[c].x);
-        acc[c].y = fma(pv[u][c].y, xi[u], acc[c].y);
-      }
-    }
-  }
-}
-
 // Issue this thread's chunks of row il into the ring slot at smem byte
 // address `dst`, then commit one group (possibly empty).
 __device__ __forceinline__ void ring_fill(const PlanView& v, const double* src_row, int il, int ti,
@@ -379,7 +339,7 @@ __device__ __forceinline__ void ring_fill(const PlanView& v, const double* src_r
 
 constexpr uint32_t kSlotBytes = CH * NT * 16;
 
-// Phase A over one wide tile through the ring (same sums as phase_a_tile).
+// Phase A over one tile through the ring.
 __device__ __forceinline__ void phase_a_ring(const PlanView& v, const double* fill_row, int c0,
                                              int m, int ti, int col0, double2 (&acc)[CH],
                                              const Smem& sh) {
@@ -779,23 +739,13 @@ __device__ __noinline__ void phase_a(const PlanView v, int64_t r0, int64_t r1, d
     const int ulo = s_win_lo[ti], W = s_win_hi[ti] - ulo;
     if (W <= 0) continue;
     const int col0 = ulo + 2 * t;
-    const int nch = (W + 2 * NT - 1) / (2 * NT);
     double2 acc[CH];
 #pragma unroll
     for (int c = 0; c < CH; ++c) acc[c] = make_double2(0.0, 0.0);
     for (int c0 = 0; c0 < rows; c0 += kRows) {
       const int m = min(rows - c0, kRows);
       const double* row0 = v.P + (r0 + c0) * v.ld + T;
-      if (v.mode == kPlanRing) {
-        phase_a_ring(v, row0, c0, m, ti, col0, acc, sh);
-      } else {
-        switch (nch) {
-          case 1: phase_a_tile<1>(v, row0, c0, m, ti, col0, acc, sh); break;
-          case 2: phase_a_tile<2>(v, row0, c0, m, ti, col0, acc, sh); break;
-          case 3: phase_a_tile<3>(v, row0, c0, m, ti, col0, acc, sh); break;
-          default: phase_a_tile<4>(v, row0, c0, m, ti, col0, acc, sh); break;
-        }
-      }
+      phase_a_ring(v, row0, c0, m, ti, col0, acc, sh);
     }
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
@@ -931,45 +881,8 @@ __device__ __forceinline__ double warp_reduce8(const double (&d)[8], int lane) {
   return s;
 }
 
-// Phase B over one tile for CTA rows e-1, e-2, ..., e-m (descending), in
-// batches of 8 rows: per-lane dots of the batch, one transpose-reduction, the
-// per-warp partials accumulate in sh.bp[warp][row - c0].
-template <int NCH>
-__device__ __forceinline__ void phase_b_tile(const PlanView& v, const double* row_top, int e,
-                                             int m, int c0, int ti, int col0,
-                                             const double2 (&wv)[CH], Smem& sh) {
-  constexpr int UB = NCH <= 2 ? 8 : 4;               // rows loaded at once
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int row_of_lane = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-  for (int q0 = 0; q0 < m; q0 += 8) {
-    double d8[8];
-#pragma unroll
-    for (int h = 0; h < 8; h += UB) {
-      double2 pv[UB][NCH];
-#pragma unroll
-      for (int u = 0; u < UB; ++u) {
-        const int q = q0 + h + u;
-        int lo = 0, hi = 0;
-        if (q < m) get_span(v, e - 1 - q, ti, lo, hi);
-        load_row<NCH>(row_top - int64_t(q) * v.ld, lo, hi, col0, pv[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < UB; ++u) {
-        double dot = 0.0;
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-          dot = fma(pv[u][c].x, wv[c].x, dot);
-          dot = fma(pv[u][c].y, wv[c].y, dot);
-        }
-        d8[h + u] = dot;
-      }
-    }
-    const double s = warp_reduce8(d8, lane);
-    if ((lane & 3) == 0 && q0 + row_of_lane < m) sh.bp[warp][e - 1 - (q0 + row_of_lane) - c0] += s;
-  }
-}
-
-// Phase B over one wide tile through the ring (same sums as phase_b_tile).
+// Phase B over one tile through the ring, rows descending: per-lane dots of 8
+// rows, one transpose-reduction, per-warp partials in sh.bp[warp][row - c0].
 __device__ __forceinline__ void phase_b_ring(const PlanView& v, const double* fill_row, int e,
                                              int m, int c0, int ti, int col0,
                                              const double2 (&wv)[CH], Smem& sh) {
@@ -1040,7 +953,6 @@ __device__ __noinline__ void phase_b(const PlanView v, const double* w, int64_t 
       const int ulo = s_win_lo[ti], W = s_win_hi[ti] - ulo;
       if (W <= 0) continue;
       const int col0 = ulo + 2 * t;
-      const int nch = (W + 2 * NT - 1) / (2 * NT);
       double2 wv[CH];
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
@@ -1048,16 +960,7 @@ __device__ __noinline__ void phase_b(const PlanView v, const double* w, int64_t 
         wv[c] = rel < W ? ldcg2(w + T + ulo + rel) : make_double2(0.0, 0.0);
       }
       const double* row_top = v.P + (r0 + e - 1) * v.ld + T;
-      if (v.mode == kPlanRing) {
-        phase_b_ring(v, row_top, e, m, c0, ti, col0, wv, sh);
-      } else {
-        switch (nch) {
-          case 1: phase_b_tile<1>(v, row_top, e, m, c0, ti, col0, wv, sh); break;
-          case 2: phase_b_tile<2>(v, row_top, e, m, c0, ti, col0, wv, sh); break;
-          case 3: phase_b_tile<3>(v, row_top, e, m, c0, ti, col0, wv, sh); break;
-          default: phase_b_tile<4>(v, row_top, e, m, c0, ti, col0, wv, sh); break;
-        }
-      }
+      phase_b_ring(v, row_top, e, m, c0, ti, col0, wv, sh);
     }
     __syncthreads();
     if (t < m) {
@@ -1395,29 +1298,12 @@ constexpr size_t kDynBytes = kDynRing > kDynSparse ? kDynRing : kDynSparse;
 //   part[0..G] = row boundaries of the G CTAs, part[G+1] = PlanMode.
 // Sparse (one tile, ld <= 4096): rows balanced on cost_i = nnz_i + 32, row i
 // going to CTA floor(prefix_i * G / total); used if every CTA's rows and
-// nonzeros fit its shared memory.  Otherwise equal rows (the streaming phases
-// cost ~ rows x window chunks; a span-balanced split measured slower), and
-// kPlanL2 when the sum of the row spans fits the L2 budget.
+// nonzeros fit its shared (kPlanSparse) or global (kPlanSparseG) slice.
+// Otherwise equal rows (the streaming phases cost ~ rows x window chunks; a
+// span-balanced split measured slower) and the ring.
 // ---------------------------------------------------------------------------
 constexpr int kPartThreads = 1024;
 constexpr int kPartRows = kSparseCols;               // rows handled in shared memory
-
-__device__ __forceinline__ int64_t row_span(const uint64_t* mask, int64_t ld, int64_t mw,
-                                            int64_t i) {
-  int64_t span = 0;
-  const int nt = ntiles_of(ld);
-  for (int ti = 0; ti < nt; ++ti) {
-    const uint64_t bits = __ldg(mask + i * mw + ti);
-    if (!bits) continue;
-    const int64_t T = int64_t(ti) * TILE;
-    const int64_t width = ld - T < TILE ? ld - T : int64_t(TILE);
-    const int64_t lo = int64_t(__ffsll(static_cast<long long>(bits)) - 1) * kSegCols;
-    int64_t hi = int64_t(64 - __clzll(static_cast<long long>(bits))) * kSegCols;
-    if (hi > width) hi = width;
-    span += hi - lo;
-  }
-  return span;
-}
 
 template <typename T>
 __device__ T block_sum_part(T v, T* buf) {                // all threads get the total
@@ -1439,17 +1325,12 @@ __global__ void __launch_bounds__(kPartThreads) k_partition(const uint64_t* mask
   __shared__ int64_t s_buf[32];
   __shared__ int s_ibuf[32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  int mode = n * ld * 8 <= kL2ModeBytes ? kPlanL2 : kPlanRing;
+  int mode = kPlanRing;
   bool sparse = false;
   if (mask) {
-    int64_t sp = 0, nz = 0;
-    for (int64_t i = t; i < n; i += kPartThreads) {
-      sp += row_span(mask, ld, mw, i);
-      nz += int64_t(__ldg(mask + i * mw + mw - 1));
-    }
-    sp = block_sum_part<int64_t>(sp, s_buf);
+    int64_t nz = 0;
+    for (int64_t i = t; i < n; i += kPartThreads) nz += int64_t(__ldg(mask + i * mw + mw - 1));
     nz = block_sum_part<int64_t>(nz, s_buf);
-    mode = sp * 8 <= kL2ModeBytes ? kPlanL2 : kPlanRing;
     const int64_t cap = sg_ok ? kSparseGCap : kSparseCap;
     // compressed rows pay 10 B per nonzero per pass (value + column) against
     // 8 B per span column: only below half density
