@@ -255,7 +255,7 @@ def run_ours(args, rank, world):
     }
     if not args.no_extras:
         out["extras"] = run_extras(args, rank, world, dev)
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:   # N = 1 only (contract)
         out["cpu_baseline"] = cpu_baseline(host_prob, budget_s=args.cpu_budget)
     return out
 
