@@ -59,12 +59,13 @@ __global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
   const double* crow = a.C + (valid ? row : 0) * a.ld;
   const int64_t n = a.n;
   double m = OTN_NINF, s = 0.0;
-  // the next step's four 16-byte C loads are issued before this step's math
-  double2 cur[4], nxt[4];
+  // C loads run two 256-column steps ahead of the math (cur, nxt, nx2)
+  double2 cur[4], nxt[4], nx2[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int64_t j = 64 * k + 2 * lane;
     cur[k] = valid && j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
+    nxt[k] = valid && j + 256 < n ? ld_stream2(crow + j + 256) : make_double2(0.0, 0.0);
   }
   int buf = 0;
   for (int64_t base = 0; base < n; base += 256) {
@@ -75,8 +76,8 @@ __global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
     __syncthreads();                                 // also publishes s_exp on the first step
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int64_t j = base + 256 + 64 * k + 2 * lane;
-      nxt[k] = valid && j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
+      const int64_t j = base + 512 + 64 * k + 2 * lane;
+      nx2[k] = valid && j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
     }
     double b[8];
 #pragma unroll
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
       for (int k = 0; k < 8; ++k) s += exp_tab(b[k] - m, s_exp);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) cur[k] = nxt[k];
+    for (int k = 0; k < 4; ++k) { cur[k] = nxt[k]; nxt[k] = nx2[k]; }
     buf ^= 1;
   }
   warp_lse(m, s);
