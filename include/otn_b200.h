@@ -140,7 +140,9 @@ int otn_lse_rows(otn_ctx* ctx, const double* C, double neg_gamma, const double* 
                  const double* inner, double* out);
 /* out_j = outer_j + LSE_i(neg_gamma*C_ij + inner_i) — the column reduction
  * log_plan_row_sums(K^T, v, u) of dual.py:91-102 / dual.py:186-194.  With
- * symmetric != 0 the rows of C are read instead (K^T aliases K, dual.py:80-88). */
+ * symmetric != 0 the rows of C are read instead (K^T aliases K, dual.py:80-88);
+ * a caller holding a materialized transpose (as the reference holds K^T,
+ * dual.py:77-89) passes it with symmetric = 1: a coalesced row pass.        */
 int otn_lse_cols(otn_ctx* ctx, const double* C, int symmetric, double neg_gamma,
                  const double* outer, const double* inner, double* out);
 /* v_j = log_c_j - LSE_i(neg_gamma*C_ij + u_i)   (rebalance_columns, dual.py:179-184) */

@@ -255,3 +255,16 @@ class DeviceCost:
 
     def ptr(self):
         return vptr(self.C)
+
+    def col_args(self):
+        """(matrix, symmetric flag) for a column-direction pass.  An asymmetric
+        cost gets its transpose materialized once on first use (the reference
+        forms K^T likewise, dual.py:77-89) so column log-sum-exps run as
+        coalesced row passes; a symmetric one is its own transpose."""
+        if self.symmetric:
+            return vptr(self.C), 1
+        if getattr(self, "CT", None) is None:
+            t = torch()
+            self.CT = t.zeros_like(self.C)
+            self.CT[:, : self.n].copy_(self.C[:, : self.n].t())
+        return vptr(self.CT), 1

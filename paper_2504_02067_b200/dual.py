@@ -157,7 +157,7 @@ class DualState:
 
     def _lse_cols(self, outer, inner, out):
         self._touch_KT()
-        self._ctx.call("otn_lse_cols", self._dc.ptr(), int(self._dc.symmetric), self._ng,
+        self._ctx.call("otn_lse_cols", *self._dc.col_args(), self._ng,
                        vptr(outer), vptr(inner), vptr(out))
 
     def refresh(self):
@@ -293,7 +293,7 @@ class DualState:
         opcount.add(4)
         self._touch_KT()
         mass = ctypes.c_double(0.0)
-        self._ctx.call("otn_trial_cols", self._dc.ptr(), int(self._dc.symmetric), self._ng,
+        self._ctx.call("otn_trial_cols", *self._dc.col_args(), self._ng,
                        vptr(self._u), vptr(d_u), vptr(self._v), vptr(d_v), float(alpha),
                        vptr(out), ctypes.byref(mass))
         return float(mass.value)
@@ -314,7 +314,7 @@ class DualState:
         """v = log c - LSE_cols(u); log c(P) := log c; refresh rows (dual.py:179-184)."""
         opcount.add(4)
         self._touch_KT()
-        self._ctx.call("otn_rebalance_cols", self._dc.ptr(), int(self._dc.symmetric), self._ng,
+        self._ctx.call("otn_rebalance_cols", *self._dc.col_args(), self._ng,
                        vptr(self._log_c), vptr(self._u), vptr(self._v))
         self._invalidate()
         self._ctx.copy(self._lc, self._log_c)
