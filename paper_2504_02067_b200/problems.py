@@ -278,10 +278,15 @@ def workload(spec):
     ``otf:<n>:<dim>:<seed>`` (uniform points, on-the-fly PointCloudProblem).
     """
     kind, *rest = spec.split(":")
-    if kind == "grid":
-        side, metric, seed = int(rest[0]), rest[1], int(rest[2])
-        return grid_problem(side, metric, seed)
-    n, dim, seed = int(rest[0]), int(rest[1]), int(rest[2])
+    if kind not in ("grid", "pts", "pix", "otf") or len(rest) != 3:
+        raise DomainError(f"unknown workload spec {spec!r}")
+    try:
+        if kind == "grid":
+            side, metric, seed = int(rest[0]), rest[1], int(rest[2])
+            return grid_problem(side, metric, seed)
+        n, dim, seed = int(rest[0]), int(rest[1]), int(rest[2])
+    except ValueError as exc:
+        raise DomainError(f"bad workload spec {spec!r}: {exc}") from exc
     if kind == "pts":
         return dense_points_problem(n, dim, seed, "uniform")
     if kind == "pix":
