@@ -3,21 +3,20 @@
 // cooperative kernel: one 512-thread CTA per SM, grid-wide barriers between
 // the dependent phases, no host round trip until the direction is done.
 //
-// Data layout: CTA b owns the contiguous row block [r0, r1) of the plan P.
-// A Hessian-vector product  q = rP*x - rho * P((P^T x)/cP)  is
+// Data layout: CTA b owns the contiguous row block [r0, r1) of the plan P
+// (k_partition picks the blocks and the plan mode, below).  A Hessian-vector
+// product  q = rP*x - rho * P((P^T x)/cP)  is
 //   phase A   per-CTA column partials  wpart[b][j] = sum_{i in block} P_ij x_i
-//             (rows ascending, 16-byte streaming loads, FMA accumulate)
 //   -- grid barrier --
 //   phase A2  column slices: w_j = sum_b wpart[b][j] (fixed order); wc = w/cP
 //   -- grid barrier --
-//   phase B   own rows, DESCENDING (the rows phase A touched last are still
-//             in L2): s_i = sum_j P_ij wc_j, then q_i = rP_i x_i - rho s_i.
-// The thread -> column mapping is identical in phases A and B (thread t owns
-// columns {2t, 2t+1} + k*1024 of every 4096-column tile), so each thread's
-// wc values live in registers during phase B.  512 threads x 4 chunks of 16 B
-// per row keep 64-128 KB of loads in flight per SM.
-// CG vector updates are row-local; the dot products / L1 norms are grid
-// reductions with fixed trees (deterministic, no FP64 atomics).
+//   phase B   own rows: s_i = sum_j P_ij wc_j, then q_i = rP_i x_i - rho s_i.
+// Phases A / B stream the plan (dense plans: cp.async rings over per-CTA
+// column windows) or walk compressed rows (sparse plans: CSR + local CSC in
+// shared or global memory).  Inside the CG loop the barriers are merged with
+// the CG-scalar reductions (pcg): 2 grid barriers per CG iteration.
+// CG state lives in registers (one row per thread); dot products / L1 norms
+// are grid reductions with fixed trees (deterministic, no FP64 atomics).
 #include <cooperative_groups.h>
 
 #include "otn_common.cuh"
@@ -172,7 +171,7 @@ __device__ __forceinline__ void grid_reduce_end(double (&v)[K], int& slot, Smem&
 // thread t owns window columns {2t, 2t+1} + c*1024, so for a sparse-ish plan
 // all threads work on the few nonzero columns instead of most of them idling.
 // Chunks outside the span are exact zeros and are neither loaded nor used:
-// the results equal the dense computation bit for bit.  (Register-batched
+// the results equal the dense computation.  (Register-batched
 // ld.global.cg was the faster path for L2-resident spans in isolation,
 // tools/l2stream.cu, but lost to the ring inside the kernel once the sparse
 // modes below took the late stages; it was retired.)
@@ -375,18 +374,19 @@ __device__ __forceinline__ void phase_a_ring(const PlanView& v, const double* fi
 }
 
 // ---------------------------------------------------------------------------
-// kPlanSparse: compressed rows in shared memory.
+// kPlanSparse / kPlanSparseG: compressed rows.
 //
-// At weak regularization a row of the plan holds a few dozen nonzeros (the
-// rest underflow to exact 0), far fewer than its segment span.  Each CTA then
-// extracts its rows' nonzeros once per launch (warp per row, ballot
-// compaction, column order) into a CSR in the dynamic shared memory the ring
-// would otherwise use, plus a local CSC (a permutation sorted by column, rows
-// ascending within a column, built by a counting sort).  Phase A walks the
-// CSC: each column's partial is the rows-ascending fma chain of the dense
-// phase A, bit for bit.  Phase B walks the CSR, warp per row.
-// k_partition chooses this mode and a row partition balanced on nonzeros, and
-// guarantees the capacities below.
+// At weak regularization a row of the plan holds tens to hundreds of
+// nonzeros (the rest underflow to exact 0), far fewer than its segment span.
+// Each CTA then extracts its rows' nonzeros once per launch (warp per row,
+// ballot compaction, column order) into a CSR — in the dynamic shared memory
+// the ring would otherwise use, or in a per-CTA slice of global memory — plus
+// a local CSC (rows ascending within a column, built by a counting sort; in
+// the global mode holding the values, thread-interleaved).  Phase A splits
+// the CSC entries evenly over the threads (sums per column in row order,
+// column pieces joined left to right); phase B walks the CSR, warp per row.
+// k_partition chooses these modes and a row partition balanced on nonzeros,
+// and guarantees the capacities below.
 // ---------------------------------------------------------------------------
 
 struct SparseView {
