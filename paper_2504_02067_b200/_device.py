@@ -48,12 +48,15 @@ def vptr(t):
 
 # Kernel launches issued by each C-ABI entry point (for the bench's
 # gpu_launches claim).  otn_lse_cols / otn_rebalance_cols / otn_trial_cols launch
-# one kernel for symmetric costs and two otherwise; trial adds the mass reduce.
+# one kernel for symmetric costs (or a materialized transpose) and two
+# otherwise; trial adds the mass reduce.  Every persistent-solver entry point
+# launches k_partition then k_coop.
 LAUNCHES = {
     "otn_lse_rows": 1, "otn_lse_cols": 2, "otn_rebalance_cols": 2, "otn_trial_cols": 3,
-    "otn_materialize": 1, "otn_plan_mask": 1, "otn_system_prep": 1, "otn_square_matvec": 1, "otn_matvec": 1,
-    "otn_rmatvec": 1, "otn_apply_F": 1, "otn_apply_pc": 1, "otn_pcg": 1, "otn_newton": 1,
-    "otn_vec": 1, "otn_reduce": 1, "otn_round_plan": 10, "otn_probe": 1, "otn_pc_pass": 1,
+    "otn_materialize": 1, "otn_plan_mask": 1, "otn_system_prep": 1, "otn_square_matvec": 1,
+    "otn_matvec": 2, "otn_rmatvec": 2, "otn_apply_F": 2, "otn_apply_pc": 2, "otn_pcg": 2,
+    "otn_newton": 2, "otn_probe": 2,
+    "otn_vec": 1, "otn_reduce": 1, "otn_round_plan": 10, "otn_pc_pass": 1,
     "otn_vec_n": 1, "otn_reduce_n": 1,
 }
 
