@@ -1,7 +1,8 @@
 // On-the-fly point-cloud cost (D4/D5): every O(n^2) pass
 // recomputes C_ij = (sum_k (x_ik - y_jk)^2) / C_max and the plan entry from the
 // point coordinates instead of streaming a stored matrix.  The coordinate sum
-// runs left to right with explicit roundings and the division is IEEE, so C_ij
+// runs left to right with explicit roundings and the division is correctly
+// rounded (reciprocal multiply + one FMA correction, Markstein), so C_ij
 // is bit-identical to the host-materialized cost (PointCloudProblem.
 // materialize_cost) and every exponent is formed with the stored path's
 // operand order: results match the stored-C kernels up to summation order.
@@ -25,8 +26,21 @@ constexpr int kPcMaxDim = 4;
 
 
 
-// e_ij: order 0 -> (ng*C + colpot_j) + rowpot_i ; order 1 -> (ng*C + rowpot_i) + colpot_j
-__device__ __forceinline__ double pc_cost(const double* a, const double* b, int d, double cmax) {
+// s / cmax, correctly rounded, as one multiply and two FMAs: with
+// rc = RN(1/cmax), q0 = RN(s * rc) is within one ulp of s / cmax, the
+// remainder e = s - q0 * cmax is exact in one FMA, and RN(q0 + e * rc) is the
+// correctly rounded quotient (Markstein's theorem; it needs no underflow, so
+// quotients near the subnormal range take __ddiv_rn).  Bit-identical to the
+// host's IEEE division C /= C.max() (tests/test_gpu_pointcloud.py).
+__device__ __forceinline__ double div_cmax(double s, double cmax, double rc) {
+  const double q0 = __dmul_rn(s, rc);
+  if (q0 < 0x1p-960) return __ddiv_rn(s, cmax);
+  const double e = fma(-q0, cmax, s);
+  return fma(e, rc, q0);
+}
+
+__device__ __forceinline__ double pc_cost(const double* a, const double* b, int d, double cmax,
+                                          double rc) {
   double s = 0.0;
 #pragma unroll
   for (int k = 0; k < kPcMaxDim; ++k) {
@@ -35,7 +49,7 @@ __device__ __forceinline__ double pc_cost(const double* a, const double* b, int 
       s = k == 0 ? __dmul_rn(dk, dk) : __dadd_rn(s, __dmul_rn(dk, dk));
     }
   }
-  return cmax > 0.0 ? __ddiv_rn(s, cmax) : s;
+  return cmax > 0.0 ? div_cmax(s, cmax, rc) : s;
 }
 
 template <int RW, int OP>
@@ -45,6 +59,7 @@ __global__ void __launch_bounds__(kPcThreads, 2) k_pair(PairArgs p) {
   __shared__ double svec[kPcTile];
   __shared__ double2 s_exp[64];
   exp_tab_load(s_exp);                               // made visible by the tile loop's barrier
+  const double rc = p.cmax > 0.0 ? __drcp_rn(p.cmax) : 0.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t i0 = (int64_t(blockIdx.x) * 8 + warp) * RW;
   double a[RW][kPcMaxDim], rp[RW];
@@ -91,7 +106,7 @@ __global__ void __launch_bounds__(kPcThreads, 2) k_pair(PairArgs p) {
             double bb[kPcMaxDim];
 #pragma unroll
             for (int k = 0; k < kPcMaxDim; ++k) bb[k] = sb[k][t];
-            const double c = pc_cost(a[r], bb, p.d, p.cmax);
+            const double c = pc_cost(a[r], bb, p.d, p.cmax, rc);
             e[q] = __dadd_rn(__dmul_rn(p.ng, c), scp[t]);
             if (p.rowpot) e[q] = __dadd_rn(e[q], rp[r]);
           } else {
@@ -116,7 +131,7 @@ __global__ void __launch_bounds__(kPcThreads, 2) k_pair(PairArgs p) {
         const double cpj = scp[t], vj = svec[t];
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
-          const double c = pc_cost(a[r], bb, p.d, p.cmax);
+          const double c = pc_cost(a[r], bb, p.d, p.cmax, rc);
           if (OP == OTN_PC_MAXD) {
             m[r] = fmax(m[r], c);
           } else if (OP == OTN_PC_CDOT) {

@@ -63,3 +63,26 @@ def test_otf_mdot_matches_reference_trajectory(name):
     assert sol.primal_cost == pytest.approx(meta["primal"], rel=1e-9)
     st.set_targets(pc.r, pc.c)
     assert st.grad_norm_l1() <= 2 * meta["true_marginal_err"] + 1e-12
+
+
+@pytest.mark.parametrize("n,d,scale", [(2048, 2, 1.0), (1500, 3, 1e-3), (777, 4, 1e4)])
+def test_otf_cost_bitwise(n, d, scale):
+    """The pair kernel's C_ij = D_ij / C_max (a reciprocal multiply plus an
+    FMA correction in place of a division) is bit-identical to the host's IEEE
+    division, read out through C . e_k (PC_CDOT with a one-hot vector)."""
+    import torch
+    from paper_2504_02067_b200 import _lib
+    pc = problems.points_problem(n, d, 11)
+    pc.X = pc.X * scale
+    pc.Y = pc.Y * scale
+    cost = PointCloudCost(pc, torch.device("cuda", 0))
+    C = pc.materialize_cost()
+    assert cost.cmax == pc.raw_cost_rows(0, n).max()
+    out = cost.zeros(n)
+    e = cost.zeros(n)
+    for k in np.random.default_rng(0).choice(n, 24, replace=False):
+        e.zero_()
+        e[int(k)] = 1.0
+        cost.pass_(_lib.PC_CDOT, rows_first=True, out=out, vec=e)
+        got = out.cpu().numpy()
+        np.testing.assert_array_equal(got.view(np.int64), C[:, k].view(np.int64))
