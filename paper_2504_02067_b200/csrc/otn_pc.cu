@@ -13,8 +13,9 @@
 // each staged column is reused by all the CTA's rows.  Column passes (P^T x,
 // column LSE) are the same kernel with the two point sets swapped
 // (dist(x, y) == dist(y, x) exactly) and a flag that keeps the exponent's
-// operand order ((ng*C + v_j) + u_i).  The FP64 pipe bounds it: ~40 FP64
-// instructions per entry (distance, IEEE division, exp).
+// operand order ((ng*C + v_j) + u_i).  The point dimension D (1..4) is a
+// template parameter so coordinates take exactly D registers per row.  FP64
+// issue bounds it: ~30 FP64 instructions per entry (distance, division, exp).
 #include "otn_common.cuh"
 #include "otn_internal.h"
 
@@ -22,7 +23,6 @@ namespace otn {
 
 constexpr int kPcThreads = 256;     // 8 warps
 constexpr int kPcTile = 256;        // column points per shared-memory tile
-constexpr int kPcMaxDim = 4;
 
 
 
@@ -39,22 +39,20 @@ __device__ __forceinline__ double div_cmax(double s, double cmax, double rc) {
   return fma(e, rc, q0);
 }
 
-__device__ __forceinline__ double pc_cost(const double* a, const double* b, int d, double cmax,
-                                          double rc) {
+template <int D>
+__device__ __forceinline__ double pc_cost(const double* a, const double* b, double cmax, double rc) {
   double s = 0.0;
 #pragma unroll
-  for (int k = 0; k < kPcMaxDim; ++k) {
-    if (k < d) {
-      const double dk = __dsub_rn(a[k], b[k]);
-      s = k == 0 ? __dmul_rn(dk, dk) : __dadd_rn(s, __dmul_rn(dk, dk));
-    }
+  for (int k = 0; k < D; ++k) {
+    const double dk = __dsub_rn(a[k], b[k]);
+    s = k == 0 ? __dmul_rn(dk, dk) : __dadd_rn(s, __dmul_rn(dk, dk));
   }
   return cmax > 0.0 ? div_cmax(s, cmax, rc) : s;
 }
 
-template <int RW, int OP>
-__global__ void __launch_bounds__(kPcThreads, 2) k_pair(PairArgs p) {
-  __shared__ double sb[kPcMaxDim][kPcTile];
+template <int RW, int D, int OP, int MB = 2>
+__global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
+  __shared__ double sb[D][kPcTile];
   __shared__ double scp[kPcTile];
   __shared__ double svec[kPcTile];
   __shared__ double2 s_exp[64];
@@ -62,14 +60,13 @@ __global__ void __launch_bounds__(kPcThreads, 2) k_pair(PairArgs p) {
   const double rc = p.cmax > 0.0 ? __drcp_rn(p.cmax) : 0.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t i0 = (int64_t(blockIdx.x) * 8 + warp) * RW;
-  double a[RW][kPcMaxDim], rp[RW];
+  double a[RW][D], rp[RW];
   double m[RW], s[RW];
 #pragma unroll
   for (int r = 0; r < RW; ++r) {
     const int64_t i = i0 + r;
 #pragma unroll
-    for (int k = 0; k < kPcMaxDim; ++k)
-      a[r][k] = (i < p.na && k < p.d) ? __ldg(p.A + k * p.lda + i) : 0.0;
+    for (int k = 0; k < D; ++k) a[r][k] = i < p.na ? __ldg(p.A + k * p.lda + i) : 0.0;
     rp[r] = (p.rowpot && i < p.na) ? __ldg(p.rowpot + i) : 0.0;
     m[r] = (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART || OP == OTN_PC_MAXD || OP == OTN_PC_DIAG)
                ? OTN_NINF : 0.0;
@@ -81,8 +78,7 @@ __global__ void __launch_bounds__(kPcThreads, 2) k_pair(PairArgs p) {
       const int64_t j = j0 + t;
       const bool ok = j < p.nb;
 #pragma unroll
-      for (int k = 0; k < kPcMaxDim; ++k)
-        sb[k][t] = (ok && k < p.d) ? __ldg(p.B + k * p.ldb + j) : 0.0;
+      for (int k = 0; k < D; ++k) sb[k][t] = ok ? __ldg(p.B + k * p.ldb + j) : 0.0;
       double cp = 0.0;
       if (ok && p.colpot) {
         cp = __ldg(p.colpot + j);
@@ -103,10 +99,10 @@ __global__ void __launch_bounds__(kPcThreads, 2) k_pair(PairArgs p) {
         for (int q = 0; q < 8; ++q) {
           const int t = lane + 32 * q;
           if (t < jn) {
-            double bb[kPcMaxDim];
+            double bb[D];
 #pragma unroll
-            for (int k = 0; k < kPcMaxDim; ++k) bb[k] = sb[k][t];
-            const double c = pc_cost(a[r], bb, p.d, p.cmax, rc);
+            for (int k = 0; k < D; ++k) bb[k] = sb[k][t];
+            const double c = pc_cost<D>(a[r], bb, p.cmax, rc);
             e[q] = __dadd_rn(__dmul_rn(p.ng, c), scp[t]);
             if (p.rowpot) e[q] = __dadd_rn(e[q], rp[r]);
           } else {
@@ -125,13 +121,13 @@ __global__ void __launch_bounds__(kPcThreads, 2) k_pair(PairArgs p) {
       }
     } else {
       for (int t = lane; t < jn; t += 32) {
-        double bb[kPcMaxDim];
+        double bb[D];
 #pragma unroll
-        for (int k = 0; k < kPcMaxDim; ++k) bb[k] = sb[k][t];
+        for (int k = 0; k < D; ++k) bb[k] = sb[k][t];
         const double cpj = scp[t], vj = svec[t];
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
-          const double c = pc_cost(a[r], bb, p.d, p.cmax, rc);
+          const double c = pc_cost<D>(a[r], bb, p.cmax, rc);
           if (OP == OTN_PC_MAXD) {
             m[r] = fmax(m[r], c);
           } else if (OP == OTN_PC_CDOT) {
@@ -187,16 +183,35 @@ __global__ void __launch_bounds__(kPcThreads, 2) k_pair(PairArgs p) {
   }
 }
 
+template <int RW, int D, int OP, int MB = 2>
+static cudaError_t launch_rw(const PairArgs& p, cudaStream_t st) {
+  const int64_t rows = 8 * RW;
+  k_pair<RW, D, OP, MB><<<unsigned((p.na + rows - 1) / rows), kPcThreads, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// Rows per warp / CTAs per SM (measured on B200, d = 3, n = 65536, 8192..65536
+// rows): the log-sum-exp passes keep 8 exponents per row in flight, so they
+// run 2 rows per warp at 3 CTAs per SM; the product passes reuse each staged
+// column point across 4 rows per warp at 2 CTAs per SM, dropping to 2 rows
+// when that leaves SMs idle.  8 rows per warp spills (the previous choice,
+// 1.6-1.8x slower).
+template <int D, int OP>
+static cudaError_t launch_d(const PairArgs& p, cudaStream_t st, int num_sms) {
+  if (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART || (p.na + 31) / 32 < num_sms)
+    return launch_rw<2, D, OP, 3>(p, st);
+  return launch_rw<4, D, OP, 2>(p, st);
+}
+
 template <int OP>
 static cudaError_t launch_pair_op(const PairArgs& p, cudaStream_t st, int num_sms) {
-  // fewer rows per warp when the row count cannot fill the machine twice
-  const int64_t ctas8 = (p.na + 63) / 64;
-  if (ctas8 >= 2 * num_sms) {
-    k_pair<8, OP><<<unsigned(ctas8), kPcThreads, 0, st>>>(p);
-  } else {
-    k_pair<2, OP><<<unsigned((p.na + 15) / 16), kPcThreads, 0, st>>>(p);
+  switch (p.d) {
+    case 1: return launch_d<1, OP>(p, st, num_sms);
+    case 2: return launch_d<2, OP>(p, st, num_sms);
+    case 3: return launch_d<3, OP>(p, st, num_sms);
+    case 4: return launch_d<4, OP>(p, st, num_sms);
+    default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_pair(otn_ctx* x, const PairArgs& p) {
