@@ -225,9 +225,11 @@ constexpr size_t kSparseRp = kSparseXs + kSparseCols * 8;               // int[k
 constexpr size_t kSparseCst = kSparseRp + (kSparseRows + 4) * 4;        // int[kSparseCols + 1]
 constexpr size_t kSparseVal = kSparseCst + (kSparseCols + 4) * 4;       // double[cap]
 constexpr size_t kSparseCol = kSparseVal + size_t(kSparseCap) * 8;      // u16[cap]
-constexpr size_t kSparseRow = kSparseCol + size_t(kSparseCap) * 2;      // u16[cap]
-constexpr size_t kSparsePerm = kSparseRow + size_t(kSparseCap) * 2;     // u16[cap]
-constexpr size_t kSparseBytes = kSparsePerm + size_t(kSparseCap) * 2;
+constexpr size_t kSparsePerm = kSparseCol + size_t(kSparseCap) * 2;     // u32[cap]: CSC (entry | row << 16)
+constexpr size_t kSparseBytes = kSparsePerm + size_t(kSparseCap) * 4;
+// the CSC is stored thread-interleaved (see stage_sparse): up to NT - 1 slots
+// past the entry count, so a CTA's nonzeros must leave that much room
+constexpr int kSparseNnzMax = kSparseCap - kCoopThreads;
 
 // The (row, tile) spans live in the dynamic region after what the mode uses.
 __device__ __forceinline__ uint32_t span_offset(int mode) {
@@ -381,8 +383,9 @@ __device__ __forceinline__ void phase_a_ring(const PlanView& v, const double* fi
 // Each CTA then extracts its rows' nonzeros once per launch (warp per row,
 // ballot compaction, column order) into a CSR — in the dynamic shared memory
 // the ring would otherwise use, or in a per-CTA slice of global memory — plus
-// a local CSC (rows ascending within a column, built by a counting sort; in
-// the global mode holding the values, thread-interleaved).  Phase A splits
+// a local CSC (rows ascending within a column, built by a counting sort and
+// stored thread-interleaved: in shared memory as (CSR entry, row) pairs, in
+// the global mode holding the values themselves).  Phase A splits
 // the CSC entries evenly over the threads (sums per column in row order,
 // column pieces joined left to right); phase B walks the CSR, warp per row.
 // k_partition chooses these modes and a row partition balanced on nonzeros,
@@ -395,18 +398,17 @@ struct SparseView {
   int* cst;
   double* val;                                      // CSR values (row-major, columns ascending)
   uint16_t* col;
-  uint16_t* row;                                    // row of each CSR entry (build / mode 2)
-  uint16_t* perm;                                   // mode 2: CSC order -> CSR entry
+  uint32_t* perm;                                   // mode 2: CSC slot -> CSR entry | row << 16
   double* cval;                                     // mode 3: CSC values
   uint16_t* crow;                                   // mode 3: CSC rows
   bool direct;                                      // mode 3
 };
 
 // Per-CTA slice of the global compressed-rows buffer (kPlanSparseG):
-// val, cval [cap] doubles, then col, row, crow [cap] u16.
+// val [cap] + cval [slot] doubles, then col [cap] + crow [slot] u16.
 constexpr int kSparseGCap = 49152;                  // nonzeros per CTA (u16 CSC offsets)
 constexpr int kSparseGSlot = kSparseGCap + kCoopThreads;   // interleaved CSC: + one row of padding
-constexpr size_t kSparseGBytes = size_t(kSparseGCap) * (8 + 2 + 2) + size_t(kSparseGSlot) * (8 + 2);
+constexpr size_t kSparseGBytes = size_t(kSparseGCap) * (8 + 2) + size_t(kSparseGSlot) * (8 + 2);
 
 __device__ __forceinline__ SparseView sparse_view(void* sg) {
   char* b = reinterpret_cast<char*>(s_ring);
@@ -419,15 +421,13 @@ __device__ __forceinline__ SparseView sparse_view(void* sg) {
     v.val = reinterpret_cast<double*>(g);
     v.cval = v.val + kSparseGCap;
     v.col = reinterpret_cast<uint16_t*>(v.cval + kSparseGSlot);
-    v.row = v.col + kSparseGCap;
-    v.crow = v.row + kSparseGCap;
+    v.crow = v.col + kSparseGCap;
     v.perm = nullptr;
     v.direct = true;
   } else {
     v.val = reinterpret_cast<double*>(b + kSparseVal);
     v.col = reinterpret_cast<uint16_t*>(b + kSparseCol);
-    v.row = reinterpret_cast<uint16_t*>(b + kSparseRow);
-    v.perm = reinterpret_cast<uint16_t*>(b + kSparsePerm);
+    v.perm = reinterpret_cast<uint32_t*>(b + kSparsePerm);
     v.cval = nullptr;
     v.crow = nullptr;
     v.direct = false;
@@ -508,10 +508,10 @@ __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* 
         const unsigned bx = __ballot_sync(0xffffffffu, nx), by = __ballot_sync(0xffffffffu, ny);
         int q = pos + __popc(bx & lt) + __popc(by & lt);
         if (nx) {
-          if (q < end) { sp.val[q] = pv[u].x; sp.col[q] = uint16_t(j); sp.row[q] = uint16_t(r); }
+          if (q < end) { sp.val[q] = pv[u].x; sp.col[q] = uint16_t(j); }
           ++q;
         }
-        if (ny && q < end) { sp.val[q] = pv[u].y; sp.col[q] = uint16_t(j + 1); sp.row[q] = uint16_t(r); }
+        if (ny && q < end) { sp.val[q] = pv[u].y; sp.col[q] = uint16_t(j + 1); }
         pos += __popc(bx) + __popc(by);
       }
     }
@@ -533,11 +533,13 @@ __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* 
     if (t == 0) s_kb[NT] = E;
     __syncthreads();
   }
-  if (sp.direct) {
-    // global CSC values: rows descending, each row's (distinct) columns in
-    // parallel, cst[] as a decrementing cursor -> rows ascending per column.
-    // Stored thread-interleaved: entry k of thread t's range at
-    // (k - s_kb[t]) * split + t, so phase A's loads are coalesced.
+  {
+    // CSC placement: rows descending, each row's (distinct) columns in
+    // parallel, cst[] as a decrementing cursor -> rows ascending within every
+    // column, deterministically.  Stored thread-interleaved: entry k of
+    // thread t's range at (k - s_kb[t]) * split + t, so phase A's loads are
+    // consecutive across a warp.  Mode 3 stores the values themselves (global
+    // memory), mode 2 the CSR entry and its row (shared memory).
     const int split = s_split;
     for (int r = rows - 1; r >= 0; --r) {
       for (int e = sp.rp[r] + t; e < sp.rp[r + 1]; e += NT) {
@@ -546,30 +548,17 @@ __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* 
         while (o + 1 < split && s_kb[o + 1] <= k) ++o;
         while (s_kb[o] > k) --o;
         const int addr = (k - s_kb[o]) * split + o;
-        sp.cval[addr] = sp.val[e];
-        sp.crow[addr] = uint16_t(r);
+        if (sp.direct) {
+          sp.cval[addr] = sp.val[e];
+          sp.crow[addr] = uint16_t(r);
+        } else {
+          sp.perm[addr] = uint32_t(e) | (uint32_t(r) << 16);
+        }
       }
       __syncthreads();
     }
     if (t == 0) sp.cst[W] = E;                      // cst[d] = start of column d
     __syncthreads();
-  } else {
-    // place entries (slot order within a column is arbitrary here), ...
-    for (int e = t; e < E; e += NT) sp.perm[atomicSub(&sp.cst[sp.col[e] - ulo], 1) - 1] = uint16_t(e);
-    __syncthreads();
-    if (t == 0) sp.cst[W] = E;                      // cst[d] = start of column d
-    __syncthreads();
-    // ... then sort each column by entry index = by row (CSR is row-major):
-    // the rows-ascending order of the dense phase A, independent of the atomics.
-    for (int d = t; d < W; d += NT) {
-      const int k0 = sp.cst[d], k1 = sp.cst[d + 1];
-      for (int k = k0 + 1; k < k1; ++k) {
-        const uint16_t key = sp.perm[k];
-        int m = k - 1;
-        while (m >= k0 && sp.perm[m] > key) { sp.perm[m + 1] = sp.perm[m]; --m; }
-        sp.perm[m + 1] = key;
-      }
-    }
   }
   // Compact the nonempty columns in place of cst: cptr[m] (u16 start of the
   // m-th nonempty column, cptr[nzc] = E) and ccol[m] (its window column).
@@ -621,7 +610,7 @@ __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* 
 // Deterministic: the split depends only on the entry count.
 __device__ void phase_a_sparse(void* sg, int64_t r0, int64_t r1, double* wrow, Smem& sh) {
   const SparseView sp = sparse_view(sg);
-  const int t = threadIdx.x, rows = int(r1 - r0);
+  const int t = threadIdx.x;
   const uint16_t* cptr = reinterpret_cast<const uint16_t*>(sp.cst);
   const uint16_t* ccol = cptr + (kSparseCols + 2);
   double* head = &sh.bp[0][0];                      // per-thread piece of a column begun earlier
@@ -648,14 +637,14 @@ __device__ void phase_a_sparse(void* sg, int64_t r0, int64_t r1, double* wrow, S
         pv[u] = 0.0;
         xv[u] = 0.0;
         if (k < ke) {
+          const int ad = (k - kb) * S + t;
           if (sp.direct) {
-            const int ad = (k - kb) * S + t;
             pv[u] = sp.cval[ad];
             xv[u] = xs[sp.crow[ad]];
           } else {
-            const int e = sp.perm[k];
-            pv[u] = sp.val[e];
-            xv[u] = xs[sp.row[e]];
+            const uint32_t pe = sp.perm[ad];
+            pv[u] = sp.val[pe & 0xffffu];
+            xv[u] = xs[pe >> 16];
           }
         }
       }
@@ -1379,7 +1368,7 @@ __global__ void __launch_bounds__(kPartThreads) k_partition(const uint64_t* mask
     for (int b = t; b < G; b += kPartThreads) {
       const int r0 = part[b], r1 = part[b + 1];
       const int rows = r1 - r0, nnz = s_pref[r1] - s_pref[r0] - 32 * rows;
-      if (rows > kSparseRows || nnz > kSparseCap) bad_smem = 1;
+      if (rows > kSparseRows || nnz > kSparseNnzMax) bad_smem = 1;
       if (rows > kSparseRows || nnz > kSparseGCap || !sg_ok) bad_glob = 1;
     }
     const int no_smem = block_sum_part<int>(bad_smem, s_ibuf);

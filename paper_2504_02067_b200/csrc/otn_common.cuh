@@ -121,8 +121,10 @@ __device__ __forceinline__ void exp_tab_load(double2* tab) {
   for (int i = threadIdx.x; i < 64; i += blockDim.x) tab[i] = __ldg(&kExp2Tab[i]);
 }
 
-__device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ tab) {
-  x = x < -746.0 ? -746.0 : (x > 710.0 ? 710.0 : x);
+// exp_tab without the range clamp: x in [-746, 710] (or NaN).  Callers that
+// already know x >= -746 (they skip x < -746, whose exp is exactly 0: a
+// warp whose entries all underflow issues no exp at all) and x <= 710.
+__device__ __forceinline__ double exp_tab_nc(double x, const double2* __restrict__ tab) {
   const double t = fma(x, kExpTabC[0], 6755399441055744.0);   // 64/ln2, 1.5*2^52 shifter
   const int k = __double2loint(t);
   const double kd = t - 6755399441055744.0;
@@ -138,6 +140,17 @@ __device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ 
   const double y = tj.x + fma(tj.x, q, tj.y);        // 2^(j/64) e^r, one final rounding
   const int e = k >> 6, e1 = e >> 1;
   return (y * pow2i(e1)) * pow2i(e - e1);
+}
+
+__device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ tab) {
+  return exp_tab_nc(x < -746.0 ? -746.0 : (x > 710.0 ? 710.0 : x), tab);
+}
+
+// s + exp(x) for x <= 0 (log-sum-exp accumulation against a running max):
+// entries below -746 add an exact 0 and are skipped; NaN propagates.
+__device__ __forceinline__ double add_exp_le0(double s, double x, const double2* __restrict__ tab) {
+  if (!(x < -746.0)) s += exp_tab_nc(x, tab);
+  return s;
 }
 
 __device__ __forceinline__ double warp_sum(double v) {

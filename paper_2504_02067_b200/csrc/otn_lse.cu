@@ -59,21 +59,35 @@ __global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
   const double* crow = a.C + (valid ? row : 0) * a.ld;
   const int64_t n = a.n;
   double m = OTN_NINF, s = 0.0;
-  // C loads run two 256-column steps ahead of the math (cur, nxt, nx2)
+  // C loads run two 256-column steps ahead of the math (cur, nxt, nx2); the
+  // inner vector's next step is loaded one step ahead (raw values: the
+  // alpha * dir term is formed when staged)
+  constexpr int kIn = 256 / kLseRowThreads;
   double2 cur[4], nxt[4], nx2[4];
+  double ib[kIn], id[kIn];
+  auto load_in = [&](int64_t base) {
+#pragma unroll
+    for (int q = 0; q < kIn; ++q) {
+      const int64_t j = base + threadIdx.x + kLseRowThreads * q;
+      ib[q] = j < n ? __ldg(a.inner + j) : 0.0;
+      id[q] = a.inner_d && j < n ? __ldg(a.inner_d + j) : 0.0;
+    }
+  };
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int64_t j = 64 * k + 2 * lane;
     cur[k] = valid && j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
     nxt[k] = valid && j + 256 < n ? ld_stream2(crow + j + 256) : make_double2(0.0, 0.0);
   }
+  load_in(0);
   int buf = 0;
   for (int64_t base = 0; base < n; base += 256) {
-    for (int jj = threadIdx.x; jj < 256; jj += kLseRowThreads) {
-      const int64_t j = base + jj;
-      s_in[buf][jj] = j < n ? eff(a.inner, a.inner_d, a.alpha, j) : 0.0;
-    }
+#pragma unroll
+    for (int q = 0; q < kIn; ++q)   // numpy: base + alpha*dir, each operation rounded (dual.py:174-175)
+      s_in[buf][threadIdx.x + kLseRowThreads * q] =
+          a.inner_d ? __dadd_rn(ib[q], __dmul_rn(a.alpha, id[q])) : ib[q];
     __syncthreads();                                 // also publishes s_exp on the first step
+    if (base + 256 < n) load_in(base + 256);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t j = base + 512 + 64 * k + 2 * lane;
@@ -97,7 +111,7 @@ __global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
     }
     if (m != OTN_NINF) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) s += exp_tab(b[k] - m, s_exp);
+      for (int k = 0; k < 8; ++k) s = add_exp_le0(s, b[k] - m, s_exp);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) { cur[k] = nxt[k]; nxt[k] = nx2[k]; }
@@ -147,11 +161,11 @@ __global__ void __launch_bounds__(kLseThreads) k_lse_cols_part(LseArgs a, int64_
     if (cm1 > m1) { s1 = s1 * exp_tab(m1 - cm1, s_exp); m1 = cm1; }
     if (m0 != OTN_NINF) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) s0 += exp_tab(b0[k] - m0, s_exp);
+      for (int k = 0; k < 4; ++k) s0 = add_exp_le0(s0, b0[k] - m0, s_exp);
     }
     if (m1 != OTN_NINF) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) s1 += exp_tab(b1[k] - m1, s_exp);
+      for (int k = 0; k < 4; ++k) s1 = add_exp_le0(s1, b1[k] - m1, s_exp);
     }
   }
   sm_m[warp][2 * lane] = m0;
