@@ -199,8 +199,8 @@ def run_ours(args, rank, world):
 
     # ---- roofline of the dominant kernel -------------------------------------
     nn8 = float(n) * n * 8.0            # one pass over the n x n float64 plan
-    alg_bytes = sum(2.0 * nn8 * h + nn8 * dv for (_, _, h, dv, _) in coop)
-    coop_ms = sum(a.elapsed_time(b) for (a, b, _, _, _) in coop)
+    alg_bytes = sum(2.0 * nn8 * h + nn8 * dv for (_, h, dv, _) in coop)
+    coop_ms = sum(ms for (ms, _, _, _) in coop)
     hbm, hbm_src = peaks()
     achieved = alg_bytes / (coop_ms * 1e-3) / 1e9 if coop_ms > 0 else 0.0
     traffic = traffic_ratio = None

@@ -66,7 +66,8 @@ enum otn_vec_op {
   OTN_VEC_LSE_FIN_SUB = 14, /* out = a - (b finite ? b + log(c) : -inf)  dual.py:182        */
   OTN_VEC_ROUND_SCALE = 15, /* out = b > 0 ? min(1, a / b) : 1          driver.py:193,198     */
   OTN_VEC_SUB_MUL = 16, /* out = a - b*c              driver.py:201-202                     */
-  OTN_VEC_MUL = 17      /* out = a * b                newton.py:102                         */
+  OTN_VEC_MUL = 17,     /* out = a * b                newton.py:102                         */
+  OTN_VEC_COPY = 18     /* out = a                    dual.py:183 (log c(P) := log c)       */
 };
 
 /* Reductions for otn_reduce; results go to host_out[0..1]. */
@@ -209,6 +210,37 @@ int otn_newton(otn_ctx* ctx, const double* P, const uint64_t* seg_mask, const do
                const double* cP, const double* mu, const double* g, double eta, double rho0,
                int zero_init, int64_t max_iters, double* d_u, double* d_v,
                otn_solve_result* host_res);
+
+/* One projector Newton step with its first line-search trial and, when that
+ * trial is accepted, the accept path — all enqueued back to back, one host
+ * synchronization (projector.py:196-238 for alpha = 1).  Runs otn_newton;
+ * then, if the status is OK and the slope positive, the trial column sums at
+ * alpha = 1 into `trial` (as otn_trial_cols on (C_cols, symmetric),
+ * projector.py:122-126; the row LSE below reads C) and their
+ * mass; then, only if the full step passes the mass-form Armijo test with
+ * (armijo_c1, slope_floor) (projector.py:215-217: no backtracking), the
+ * accept path: u += d_u; v = (v + d_v) + (log_c - trial); lc := log_c;
+ * lr = row LSE (u, v) (dual.py:203-208); grad = exp(lr) - r; row statistics
+ * as OTN_RED_ROW_STATS on (lr, r).  Device-side flags gate the launches, so
+ * a step that must backtrack (or falls back) leaves u, v, lc, lr untouched
+ * and the host continues exactly as after otn_newton + otn_trial_cols.
+ * host_out = {mass, row-stats[0], row-stats[1], trial ran (0/1),
+ * accepted (0/1)}; host_flags[0] = row-stats flags.  Returns the Newton
+ * status like otn_newton.                                                    */
+int otn_newton_step(otn_ctx* ctx, const double* P, const uint64_t* seg_mask, const double* rP,
+                    const double* cP, const double* mu, const double* g, double eta, double rho0,
+                    int zero_init, int64_t max_iters, double* d_u, double* d_v, const double* C,
+                    const double* C_cols, int symmetric, double neg_gamma, double* u, double* v,
+                    const double* r,
+                    const double* log_c, double* trial, double* lc, double* lr, double* grad,
+                    double armijo_c1, double slope_floor, otn_solve_result* host_res,
+                    double* host_out, int* host_flags);
+
+/* Telemetry: with timing on, every persistent-solver launch (the partition
+ * kernel + k_coop) is bracketed by CUDA events; otn_coop_ms waits for the
+ * last one and returns its device time in milliseconds.                      */
+int otn_set_timing(otn_ctx* ctx, int on);
+int otn_coop_ms(otn_ctx* ctx, float* ms);
 
 /* Diagnostic: run building block `what` of the persistent solver `reps` times
  * in one launch (0 grid barrier, 1 grid reduction, 2 column-partial pass,

@@ -56,6 +56,8 @@ LAUNCHES = {
     "otn_materialize": 1, "otn_plan_mask": 1, "otn_system_prep": 1, "otn_square_matvec": 1,
     "otn_matvec": 2, "otn_rmatvec": 2, "otn_apply_F": 2, "otn_apply_pc": 2, "otn_pcg": 2,
     "otn_newton": 2, "otn_probe": 2,
+    # newton (2) + gate + trial (1 | 2) + mass + gate + u, v, lc + row LSE + grad + row stats
+    "otn_newton_step": 13,
     "otn_vec": 1, "otn_reduce": 1, "otn_round_plan": 10, "otn_pc_pass": 1,
     "otn_vec_n": 1, "otn_reduce_n": 1,
 }
@@ -74,11 +76,12 @@ class Telemetry:
         self.calls = {}
         self.h2d = 0
         self.d2h = 0
-        self.coop = []        # (start_event, end_event, hvps, n)
+        self.coop = []        # (device ms, hvps, d_v formed, n) per timed k_coop launch
 
     def count(self, name, sym=False):
         k = LAUNCHES.get(name, 0)
-        if sym and name in ("otn_lse_cols", "otn_rebalance_cols", "otn_trial_cols"):
+        if sym and name in ("otn_lse_cols", "otn_rebalance_cols", "otn_trial_cols",
+                            "otn_newton_step"):
             k -= 1
         self.launches += k
         self.calls[name] = self.calls.get(name, 0) + 1
@@ -86,6 +89,8 @@ class Telemetry:
 
 TELEMETRY = Telemetry()
 _SYM_CALLS = ("otn_lse_cols", "otn_rebalance_cols", "otn_trial_cols")
+_SYM_ARG = {name: 1 for name in _SYM_CALLS}
+_SYM_ARG["otn_newton_step"] = 14
 
 
 def is_tensor(x):
@@ -138,6 +143,20 @@ class Context:
                 self.lib.otn_destroy(self.h)
         except Exception:
             pass
+
+    def coop_timing(self):
+        """Match the library's launch timing to TELEMETRY.time_coop; returns it."""
+        on = bool(TELEMETRY.time_coop)
+        if getattr(self, "_timing", False) != on:
+            _lib.check(self.lib.otn_set_timing(self.h, int(on)), "otn_set_timing")
+            self._timing = on
+        return on
+
+    def coop_ms(self):
+        """Device time of the last persistent-solver launch (timing on)."""
+        ms = ctypes.c_float(0.0)
+        _lib.check(self.lib.otn_coop_ms(self.h, ctypes.byref(ms)), "otn_coop_ms")
+        return float(ms.value)
 
     # ---- buffers ---------------------------------------------------------
     def vec(self, init=None):
@@ -216,7 +235,8 @@ class Context:
 
     # ---- thin call helpers -----------------------------------------------
     def call(self, name, *args):
-        TELEMETRY.count(name, sym=bool(args[1]) if name in _SYM_CALLS else False)
+        i = _SYM_ARG.get(name)
+        TELEMETRY.count(name, sym=bool(args[i]) if i is not None else False)
         rc = getattr(self.lib, name)(self.h, *args)
         return _lib.check(rc, name)
 

@@ -37,7 +37,7 @@ OTN_ST_DOMAIN = 16
 
 (VEC_ADD_SUB, VEC_AXPY, VEC_STEP_V, VEC_EXTRAP, VEC_EXP, VEC_GRAD, VEC_MUL_SUB, VEC_DIV,
  VEC_SUB, VEC_ADD, VEC_PRECOND, VEC_NEG_DIV, VEC_RESCALE, VEC_LSE_FIN, VEC_LSE_FIN_SUB,
- VEC_ROUND_SCALE, VEC_SUB_MUL, VEC_MUL) = range(18)
+ VEC_ROUND_SCALE, VEC_SUB_MUL, VEC_MUL, VEC_COPY) = range(19)
 (RED_ROW_STATS, RED_GRAD_L1, RED_SUM_EXP, RED_DOT, RED_L1, RED_L1_ADD, RED_NONPOS,
  RED_MAX, RED_L1_DOT) = range(9)
 PC_LSE, PC_DOT, PC_DIAG, PC_MAXD, PC_LSE_PART, PC_DOTC, PC_CDOT = range(7)
@@ -73,6 +73,8 @@ SIGNATURES = {
     "otn_set_stream": [_P, _P],
     "otn_info": [_P, ctypes.POINTER(_I64)],
     "otn_read_flags": [_P, _IP],
+    "otn_set_timing": [_P, _I],
+    "otn_coop_ms": [_P, ctypes.POINTER(ctypes.c_float)],
     "otn_copy": [_P, _P, _P, _I64],
     "otn_upload": [_P, _P, _P, _I64],
     "otn_lse_rows": [_P, _P, _D, _P, _P, _P],
@@ -90,6 +92,8 @@ SIGNATURES = {
     "otn_pcg": [_P, _P, _P, _P, _P, _P, _D, _P, _D, _P, _I, _I64, ctypes.POINTER(SolveResult)],
     "otn_newton": [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I, _I64, _P, _P,
                    ctypes.POINTER(SolveResult)],
+    "otn_newton_step": [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I, _I64, _P, _P, _P, _P, _I, _D, _P, _P,
+                        _P, _P, _P, _P, _P, _P, _D, _D, ctypes.POINTER(SolveResult), _DP, _IP],
     "otn_probe": [_P, _P, _P, _P, _P, _P, _P, _I, _I64],
     "otn_coop_layout": [_P],
     "otn_pc_pass": [_P, _I, _P, _I64, _I64, _P, _I64, _I64, _I, _D, _D, _I, _P, _P, _D, _P, _P,

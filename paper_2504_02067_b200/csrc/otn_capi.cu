@@ -181,6 +181,8 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
   e = cudaMallocHost((void**)&x->h_scal, 64 * sizeof(double));
   if (e == cudaSuccess) e = cudaMallocHost((void**)&x->h_flags, 16 * sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost((void**)&x->h_res, sizeof(otn::DevResult));
+  if (e == cudaSuccess) e = cudaEventCreate(&x->ev_coop[0]);
+  if (e == cudaSuccess) e = cudaEventCreate(&x->ev_coop[1]);
   if (e != cudaSuccess) { otn_destroy(x); return fail(OTN_ERR_CUDA, "otn_create: pinned host", e); }
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { otn_destroy(x); return fail(OTN_ERR_CUDA, "otn_create: sync", e); }
@@ -195,6 +197,8 @@ int otn_destroy(otn_ctx* x) {
   if (x->h_scal) cudaFreeHost(x->h_scal);
   if (x->h_flags) cudaFreeHost(x->h_flags);
   if (x->h_res) cudaFreeHost(x->h_res);
+  if (x->ev_coop[0]) cudaEventDestroy(x->ev_coop[0]);
+  if (x->ev_coop[1]) cudaEventDestroy(x->ev_coop[1]);
   delete x;
   return OTN_OK;
 }
@@ -231,6 +235,20 @@ int otn_upload(otn_ctx* x, double* dst, const double* host_src, int64_t n) {
 int otn_coop_layout(otn_ctx* x, int* host) {
   OTN_REQUIRE(x && host, "otn_coop_layout: NULL argument");
   return sync_copy(x, host, x->part, size_t(x->coop_blocks + 2) * sizeof(int), "otn_coop_layout");
+}
+
+int otn_set_timing(otn_ctx* x, int on) {
+  OTN_REQUIRE(x, "otn_set_timing: NULL context");
+  x->time_coop = on != 0;
+  return OTN_OK;
+}
+
+int otn_coop_ms(otn_ctx* x, float* ms) {
+  OTN_REQUIRE(x && ms, "otn_coop_ms: NULL argument");
+  OTN_REQUIRE(x->time_coop, "otn_coop_ms: timing is off (otn_set_timing)");
+  OTN_CUDA(cudaEventSynchronize(x->ev_coop[1]), "otn_coop_ms: sync");
+  OTN_CUDA(cudaEventElapsedTime(ms, x->ev_coop[0], x->ev_coop[1]), "otn_coop_ms");
+  return OTN_OK;
 }
 
 int otn_read_flags(otn_ctx* x, int* host4) {
@@ -420,6 +438,76 @@ int otn_newton(otn_ctx* x, const double* P, const uint64_t* m, const double* rP,
   return finish_solve(x, host_res, "otn_newton: result");
 }
 
+int otn_newton_step(otn_ctx* x, const double* P, const uint64_t* m, const double* rP,
+                    const double* cP, const double* mu, const double* g, double eta, double rho0,
+                    int zero_init, int64_t max_iters, double* d_u, double* d_v, const double* C,
+                    const double* Ccols, int sym, double ng, double* u, double* v, const double* r,
+                    const double* log_c,
+                    double* trial, double* lc, double* lr, double* grad, double armijo_c1,
+                    double slope_floor, otn_solve_result* host_res, double* host_out,
+                    int* host_flags) {
+  OTN_REQUIRE(x && P && rP && cP && mu && g && d_u && d_v && C && Ccols && u && v && r && log_c &&
+                  trial &&
+                  lc && lr && grad && host_out,
+              "otn_newton_step: NULL argument");
+  OTN_REQUIRE(max_iters >= 0, "otn_newton_step: max_iters < 0");
+  otn::CoopArgs a = plan_args(x, P, m);
+  a.mode = otn::kModeNewton;
+  a.rP = rP;
+  a.cP = cP;
+  a.mu = mu;
+  a.g = g;
+  a.eta = eta;
+  a.rho0 = rho0;
+  a.zero_init = zero_init;
+  a.max_iters = max_iters;
+  a.d = d_u;
+  a.dv = d_v;
+  a.pre_flags = x->flags;
+  OTN_CUDA(otn::launch_coop(x, a), "otn_newton_step");
+  // scalars: scal[32] trial mass, scal[33..34] row statistics;
+  // flags[6] trial gate, flags[7] accept gate, flags[8] row-statistics flags
+  int* gates = x->flags + 6;
+  const int n = int(x->n);
+  OTN_CUDA(otn::launch_step_gate(x, 0, x->dres, nullptr, slope_floor, armijo_c1, gates),
+           "otn_newton_step: gate");
+  cudaError_t e = sym ? otn::launch_lse_rows(x, Ccols, ng, v, d_v, u, d_u, 1.0, 0, trial, gates)
+                      : otn::launch_lse_cols(x, Ccols, ng, v, d_v, u, d_u, 1.0, 0, trial, gates);
+  OTN_CUDA(e, "otn_newton_step: trial");
+  OTN_CUDA(otn::launch_reduce(x, OTN_RED_SUM_EXP, n, trial, nullptr, nullptr, nullptr,
+                              x->scal + 32, x->flags + 4, gates),
+           "otn_newton_step: mass");
+  OTN_CUDA(otn::launch_step_gate(x, 1, x->dres, x->scal + 32, slope_floor, armijo_c1, gates),
+           "otn_newton_step: armijo");
+  const int* acc = gates + 1;
+  OTN_CUDA(otn::launch_vec(x, OTN_VEC_AXPY, n, 1.0, u, d_u, nullptr, nullptr, u, acc),
+           "otn_newton_step: u");
+  OTN_CUDA(otn::launch_vec(x, OTN_VEC_STEP_V, n, 1.0, v, d_v, log_c, trial, v, acc),
+           "otn_newton_step: v");
+  OTN_CUDA(otn::launch_vec(x, OTN_VEC_COPY, x->ld, 0.0, log_c, nullptr, nullptr, nullptr, lc, acc),
+           "otn_newton_step: lc");
+  OTN_CUDA(otn::launch_lse_rows(x, C, ng, u, nullptr, v, nullptr, 0.0, 0, lr, acc),
+           "otn_newton_step: rows");
+  OTN_CUDA(otn::launch_vec(x, OTN_VEC_GRAD, n, 0.0, lr, r, nullptr, nullptr, grad, acc),
+           "otn_newton_step: grad");
+  OTN_CUDA(otn::launch_reduce(x, OTN_RED_ROW_STATS, n, lr, r, nullptr, nullptr, x->scal + 33,
+                              x->flags + 8, acc),
+           "otn_newton_step: row stats");
+  OTN_CUDA(cudaMemcpyAsync(x->h_scal + 32, x->scal + 32, 3 * sizeof(double),
+                           cudaMemcpyDeviceToHost, x->stream), "otn_newton_step: copy");
+  OTN_CUDA(cudaMemcpyAsync(x->h_flags + 6, x->flags + 6, 3 * sizeof(int), cudaMemcpyDeviceToHost,
+                           x->stream), "otn_newton_step: copy");
+  int rc = finish_solve(x, host_res, "otn_newton_step: result");
+  const bool ran = x->h_flags[6] != 0, ok = x->h_flags[7] != 0;
+  host_out[0] = ran ? x->h_scal[32] : 0.0;
+  host_out[1] = ok ? x->h_scal[33] : 0.0;
+  host_out[2] = ok ? x->h_scal[34] : 0.0;
+  host_out[3] = ran ? 1.0 : 0.0;
+  host_out[4] = ok ? 1.0 : 0.0;
+  if (host_flags) host_flags[0] = ok ? x->h_flags[8] : 0;
+  return rc;
+}
+
 int otn_probe(otn_ctx* x, const double* P, const uint64_t* m, const double* cP, const double* rP,
               const double* xin, double* out, int what, int64_t reps) {
   OTN_REQUIRE(x && P && cP && rP && xin && out, "otn_probe: NULL argument");
@@ -457,7 +545,7 @@ int otn_pc_pass(otn_ctx* x, int op, const double* A, int64_t na, int64_t lda, co
 int otn_vec_n(otn_ctx* x, int64_t n, int op, double s, const double* a, const double* b,
               const double* c, const double* d, double* out) {
   OTN_REQUIRE(x && a && out && n >= 0, "otn_vec_n: bad argument");
-  OTN_REQUIRE(op >= OTN_VEC_ADD_SUB && op <= OTN_VEC_MUL, "otn_vec_n: bad op");
+  OTN_REQUIRE(op >= OTN_VEC_ADD_SUB && op <= OTN_VEC_COPY, "otn_vec_n: bad op");
   if (n == 0) return OTN_OK;
   OTN_CUDA(otn::launch_vec(x, op, n, s, a, b, c, d, out), "otn_vec_n");
   return OTN_OK;
@@ -484,7 +572,7 @@ int otn_reduce_n(otn_ctx* x, int64_t n, int op, const double* a, const double* b
 int otn_vec(otn_ctx* x, int op, double s, const double* a, const double* b, const double* c,
             const double* d, double* out) {
   OTN_REQUIRE(x && a && out, "otn_vec: NULL argument");
-  OTN_REQUIRE(op >= OTN_VEC_ADD_SUB && op <= OTN_VEC_MUL, "otn_vec: bad op");
+  OTN_REQUIRE(op >= OTN_VEC_ADD_SUB && op <= OTN_VEC_COPY, "otn_vec: bad op");
   OTN_CUDA(otn::launch_vec(x, op, x->n, s, a, b, c, d, out), "otn_vec");
   return OTN_OK;
 }

@@ -1392,13 +1392,16 @@ cudaError_t launch_coop(otn_ctx* x, const CoopArgs& a0) {
   a.stages = kRingDepth;
   a.part = x->part;
   a.sg = x->sg;
+  if (x->time_coop) cudaEventRecord(x->ev_coop[0], x->stream);
   k_partition<<<1, kPartThreads, 0, x->stream>>>(a.mask, a.n, a.ld, a.mw, x->coop_blocks,
                                                  x->sg != nullptr, x->part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
-  return cudaLaunchCooperativeKernel((void*)k_coop, dim3(x->coop_blocks), dim3(NT), args,
-                                     kDynBytes, x->stream);
+  e = cudaLaunchCooperativeKernel((void*)k_coop, dim3(x->coop_blocks), dim3(NT), args, kDynBytes,
+                                  x->stream);
+  if (e == cudaSuccess && x->time_coop) e = cudaEventRecord(x->ev_coop[1], x->stream);
+  return e;
 }
 
 size_t sparse_g_bytes_per_cta() { return kSparseGBytes; }

@@ -55,16 +55,20 @@ struct otn_ctx {
   double* h_scal;
   int* h_flags;
   otn::DevResult* h_res;
+  int time_coop;          // record ev_coop around every persistent-solver launch
+  cudaEvent_t ev_coop[2];
 };
 
 // Launchers (all stream-ordered on ctx->stream; return cudaError_t).
 namespace otn {
+// gate (nullable): a device flag; the launch does nothing when *gate == 0
+// (otn_newton_step enqueues the accept path before the host sees the result).
 cudaError_t launch_lse_rows(otn_ctx* x, const double* C, double ng, const double* outer,
                             const double* outer_d, const double* inner, const double* inner_d,
-                            double alpha, int mode, double* out);
+                            double alpha, int mode, double* out, const int* gate = nullptr);
 cudaError_t launch_lse_cols(otn_ctx* x, const double* C, double ng, const double* outer,
                             const double* outer_d, const double* inner, const double* inner_d,
-                            double alpha, int mode, double* out);
+                            double alpha, int mode, double* out, const int* gate = nullptr);
 cudaError_t launch_materialize(otn_ctx* x, const double* C, double ng, const double* u,
                                const double* v, double* P, const double* icP, const double* rP,
                                double* mu, int* flag, uint64_t* mask);
@@ -106,9 +110,15 @@ size_t sparse_g_bytes_per_cta();        // kPlanSparseG buffer slice (allocated 
 
 // Vector kernels and single-CTA reductions.
 cudaError_t launch_vec(otn_ctx* x, int op, int64_t n, double s0, const double* a, const double* b,
-                       const double* c, const double* d, double* out);
+                       const double* c, const double* d, double* out, const int* gate = nullptr);
 cudaError_t launch_reduce(otn_ctx* x, int op, int64_t n, const double* a, const double* b,
-                          const double* c, const double* d, double* dst, int* flag);
+                          const double* c, const double* d, double* dst, int* flag,
+                          const int* gate = nullptr);
+// Newton-step gates (otn_newton_step): stage 0 -> flags[0] = (status OK and
+// slope > 0), flags[2] = 0; stage 1 -> flags[1] = flags[0] and the Armijo test
+// passes at alpha = 1 (mass = *mass).
+cudaError_t launch_step_gate(otn_ctx* x, int stage, const DevResult* res, const double* mass,
+                             double slope_floor, double armijo_c1, int* flags);
 cudaError_t launch_round(otn_ctx* x, double* P, const double* C, const double* r, const double* c,
                          double* scratch_scalars, int* flag);
 

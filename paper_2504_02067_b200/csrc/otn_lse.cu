@@ -24,6 +24,7 @@ struct LseArgs {
   double alpha;
   int mode;                 // 0: out = outer + lse;  1: out = outer - lse
   double* out;
+  const int* gate;          // nullable: skip the launch when *gate == 0
 };
 
 __device__ __forceinline__ double eff(const double* base, const double* dir, double alpha,
@@ -52,6 +53,7 @@ constexpr int kLseRowThreads = 128;
 __global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
   __shared__ double2 s_exp[64];
   __shared__ double s_in[2][256];
+  if (a.gate && *a.gate == 0) return;               // uniform over the grid
   exp_tab_load(s_exp);
   const int64_t row = int64_t(blockIdx.x) * (kLseRowThreads / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -129,6 +131,7 @@ __global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kLseThreads) k_lse_cols_part(LseArgs a, int64_t slab_rows,
                                                                double* part) {
+  if (a.gate && *a.gate == 0) return;
   __shared__ double sm_m[8][kColTile];
   __shared__ double sm_s[8][kColTile];
   __shared__ double2 s_exp[64];
@@ -188,6 +191,7 @@ __global__ void __launch_bounds__(kLseThreads) k_lse_cols_part(LseArgs a, int64_
 }
 
 __global__ void k_lse_cols_fin(LseArgs a, int slabs, const double* part) {
+  if (a.gate && *a.gate == 0) return;
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= a.n) return;
   double m = OTN_NINF, s = 0.0;
@@ -346,16 +350,16 @@ static inline unsigned rows_grid(int64_t n, int threads = kLseThreads) {
 
 cudaError_t launch_lse_rows(otn_ctx* x, const double* C, double ng, const double* outer,
                             const double* outer_d, const double* inner, const double* inner_d,
-                            double alpha, int mode, double* out) {
-  LseArgs a{C, x->n, x->ld, ng, outer, outer_d, inner, inner_d, alpha, mode, out};
+                            double alpha, int mode, double* out, const int* gate) {
+  LseArgs a{C, x->n, x->ld, ng, outer, outer_d, inner, inner_d, alpha, mode, out, gate};
   k_lse_rows<<<rows_grid(x->n, kLseRowThreads), kLseRowThreads, 0, x->stream>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_lse_cols(otn_ctx* x, const double* C, double ng, const double* outer,
                             const double* outer_d, const double* inner, const double* inner_d,
-                            double alpha, int mode, double* out) {
-  LseArgs a{C, x->n, x->ld, ng, outer, outer_d, inner, inner_d, alpha, mode, out};
+                            double alpha, int mode, double* out, const int* gate) {
+  LseArgs a{C, x->n, x->ld, ng, outer, outer_d, inner, inner_d, alpha, mode, out, gate};
   const int slabs = x->lse_slabs;
   const int64_t slab_rows = (x->n + slabs - 1) / slabs;
   dim3 grid(unsigned((x->ld + kColTile - 1) / kColTile), unsigned(slabs));

@@ -9,8 +9,9 @@ namespace otn {
 // element-wise ops (operand order of the reference's numpy expressions)
 // ---------------------------------------------------------------------------
 __global__ void k_vec(int op, int64_t n, double s, const double* a, const double* b,
-                      const double* c, const double* d, double* out) {
+                      const double* c, const double* d, double* out, const int* gate) {
   __shared__ double2 s_exp[64];
+  if (gate && *gate == 0) return;                   // uniform over the grid
   if (op == OTN_VEC_EXP) {                          // uniform: the table only where it is used
     exp_tab_load(s_exp);
     __syncthreads();
@@ -39,6 +40,7 @@ __global__ void k_vec(int op, int64_t n, double s, const double* a, const double
       case OTN_VEC_ROUND_SCALE: o = b[i] > 0.0 ? fmin(1.0, __ddiv_rn(a[i], b[i])) : 1.0; break;
       case OTN_VEC_SUB_MUL: o = __dsub_rn(a[i], __dmul_rn(b[i], c[i])); break;
       case OTN_VEC_MUL: o = __dmul_rn(a[i], b[i]); break;
+      case OTN_VEC_COPY: o = a[i]; break;
       default: o = 0.0;
     }
     out[i] = o;
@@ -50,8 +52,10 @@ __global__ void k_vec(int op, int64_t n, double s, const double* a, const double
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) k_reduce(int op, int64_t n, const double* a,
                                                  const double* b, const double* c,
-                                                 const double* d, double* dst, int* flag) {
+                                                 const double* d, double* dst, int* flag,
+                                                 const int* gate) {
   __shared__ double sh[33];
+  if (gate && *gate == 0) return;
   double s0 = 0.0, s1 = 0.0;
   int f = 0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
@@ -237,15 +241,44 @@ __global__ void __launch_bounds__(256) k_round_rank1(double* P, const double* C,
 }
 
 cudaError_t launch_vec(otn_ctx* x, int op, int64_t n, double s, const double* a, const double* b,
-                       const double* c, const double* d, double* out) {
+                       const double* c, const double* d, double* out, const int* gate) {
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, 4 * x->num_sms);
-  k_vec<<<unsigned(std::max<int64_t>(blocks, 1)), 256, 0, x->stream>>>(op, n, s, a, b, c, d, out);
+  k_vec<<<unsigned(std::max<int64_t>(blocks, 1)), 256, 0, x->stream>>>(op, n, s, a, b, c, d, out,
+                                                                       gate);
   return cudaGetLastError();
 }
 
 cudaError_t launch_reduce(otn_ctx* x, int op, int64_t n, const double* a, const double* b,
-                          const double* c, const double* d, double* dst, int* flag) {
-  k_reduce<<<1, 1024, 0, x->stream>>>(op, n, a, b, c, d, dst, flag);
+                          const double* c, const double* d, double* dst, int* flag,
+                          const int* gate) {
+  k_reduce<<<1, 1024, 0, x->stream>>>(op, n, a, b, c, d, dst, flag, gate);
+  return cudaGetLastError();
+}
+
+// The projector's decisions after a Newton launch (projector.py:203-231),
+// evaluated on the device so the accept path can be enqueued behind it:
+// stage 0: the direction is usable (status OK, slope > 0: otherwise the host
+// takes the Sinkhorn fallback or raises); stage 1: the full step passes the
+// mass-form Armijo test, i.e. the backtracking loop would not run:
+//   not (slope > floor and mass - 1 > ((1 - c1) * 1) * slope)
+// with the host expression's operand order.
+__global__ void k_step_gate(int stage, const DevResult* res, const double* mass,
+                            double slope_floor, double c1, int* flags) {
+  if (threadIdx.x != 0) return;
+  if (stage == 0) {
+    flags[0] = res->status == OTN_OK && res->slope > 0.0;
+    flags[2] = 0;
+  } else {
+    const double slope = res->slope;
+    const bool backtrack =
+        slope > slope_floor && __dsub_rn(*mass, 1.0) > __dmul_rn(__dmul_rn(__dsub_rn(1.0, c1), 1.0), slope);
+    flags[1] = flags[0] && !backtrack;
+  }
+}
+
+cudaError_t launch_step_gate(otn_ctx* x, int stage, const DevResult* res, const double* mass,
+                             double slope_floor, double armijo_c1, int* flags) {
+  k_step_gate<<<1, 32, 0, x->stream>>>(stage, res, mass, slope_floor, armijo_c1, flags);
   return cudaGetLastError();
 }
 

@@ -301,6 +301,27 @@ class DualState:
     def _trial_buf(self):
         return self._trial_vec
 
+    def _tally_trial(self):
+        """Op tally of one _trial call (its pass ran inside otn_newton_step)."""
+        opcount.add(4)
+        self._touch_KT()
+
+    def _newton_step(self, sys, eta, rho0, zero_init, max_cg_iters, d_u, d_v, armijo_c1,
+                     slope_floor):
+        """Newton direction + first trial + (if accepted) accept path in one
+        synchronization (otn_newton_step); see projector.project."""
+        from .newton import _newton_step_device
+        res, mass, rowstat = _newton_step_device(self, sys, self._g, eta, rho0, zero_init,
+                                                 max_cg_iters, d_u, d_v, armijo_c1, slope_floor)
+        if rowstat is not None:
+            # the device ran _accept(1.0, d_u, d_v) + refresh_rows_only + _row_stats
+            self._cache_valid = True
+            self._rowstat = rowstat
+        return res, mass, rowstat is not None
+
+    def _tally_refresh_rows(self):
+        opcount.add(4)                              # refresh_rows_only (dual.py:203-208)
+
     def trial_log_col_sums(self, d_u, d_v, alpha):
         k = self._ctx
         du = d_u if is_tensor(d_u) else k.vec(d_u)

@@ -246,22 +246,49 @@ def _newton_device(grad_u, sys, eta, rho0, zero_init, max_cg_iters, d_u, d_v):
     if max_cg_iters is None:
         max_cg_iters = 10 * sys.n
     res = _lib.SolveResult()
-    timed = TELEMETRY.time_coop
-    if timed:
-        t = torch()
-        ev0, ev1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
-        ev0.record()
+    timed = k.coop_timing()
     k.call("otn_newton", vptr(sys._P), vptr(sys._mask), vptr(sys._rP), vptr(sys._cP),
            vptr(sys._mu()),
            vptr(grad_u), float(eta), float(rho0), int(bool(zero_init)), int(max_cg_iters),
            vptr(d_u), vptr(d_v), ctypes.byref(res))
     if timed:
-        ev1.record()
-        TELEMETRY.coop.append((ev0, ev1, int(res.hvps), int(d_v is not None), k.n))
+        TELEMETRY.coop.append((k.coop_ms(), int(res.hvps), int(d_v is not None), k.n))
     if res.pcg_calls > 0:
         sys._tally_mu()
     opcount.add(2 * int(res.hvps))
     return res
+
+
+def _newton_step_device(state, sys, grad_u, eta, rho0, zero_init, max_cg_iters, d_u, d_v,
+                        armijo_c1, slope_floor):
+    """One otn_newton_step launch sequence for a DualState: the Newton
+    direction, its trial at alpha = 1 and, when the Armijo test passes there,
+    the accept path, with one host synchronization.  Returns
+    (res, mass or None, row statistics or None); the op tally of the Newton
+    part is added here, the trial's and the refresh's by the caller."""
+    k = sys._ctx
+    if max_cg_iters is None:
+        max_cg_iters = 10 * sys.n
+    res = _lib.SolveResult()
+    out = (ctypes.c_double * 5)()
+    fl = ctypes.c_int(0)
+    timed = k.coop_timing()
+    ccols, sym = state._dc.col_args()
+    k.call("otn_newton_step", vptr(sys._P), vptr(sys._mask), vptr(sys._rP), vptr(sys._cP),
+           vptr(sys._mu()), vptr(grad_u), float(eta), float(rho0), int(bool(zero_init)),
+           int(max_cg_iters), vptr(d_u), vptr(d_v), state._dc.ptr(), ccols, sym, state._ng,
+           vptr(state._u), vptr(state._v), vptr(state._r), vptr(state._log_c),
+           vptr(state._trial_vec), vptr(state._lc), vptr(state._lr), vptr(state._g),
+           float(armijo_c1), float(slope_floor), ctypes.byref(res), out, ctypes.byref(fl))
+    if timed:
+        TELEMETRY.coop.append((k.coop_ms(), int(res.hvps), 1, k.n))
+    if res.pcg_calls > 0:
+        sys._tally_mu()
+    opcount.add(2 * int(res.hvps))
+    opcount.add(1)                           # d_v = -apply_pc(d_u)  (projector.py:201)
+    mass = float(out[0]) if out[3] else None
+    rowstat = (float(out[1]), float(out[2]), int(fl.value)) if out[4] else None
+    return res, mass, rowstat
 
 
 def newton_solve(grad_u, sys, eta, rho0=0.0, zero_init=False, max_cg_iters=None):

@@ -17,25 +17,26 @@ p = ot.workload(spec)
 dp = ot.Problem(C=torch.from_numpy(p.C).cuda(), r=p.r, c=p.c)
 ot.mdot(dp, 2.0 ** 5, gf)          # warm
 rows = []
-orig = nt._newton_device
 
 
-def wrapped(grad_u, sys_, *a):
-    TELEMETRY.time_coop = True
-    n0 = len(TELEMETRY.coop)
-    res = orig(grad_u, sys_, *a)
-    ev0, ev1, h, dv, n = TELEMETRY.coop[n0]
-    ev1.synchronize()
-    k = sys_._ctx
-    lay = np.zeros(k.coop_blocks + 2, dtype=np.int32)
-    k.call("otn_coop_layout", lay.ctypes.data)
-    m = sys_._mask.cpu().numpy()
-    rows.append((int(lay[-1]), int(np.diff(lay[:-1]).max()), int(m[:, -1].sum()), h,
-                 ev0.elapsed_time(ev1) * 1e3))
-    return res
+def wrap(orig, sys_pos):
+    def wrapped(*a):
+        TELEMETRY.time_coop = True
+        n0 = len(TELEMETRY.coop)
+        res = orig(*a)
+        ms, h, dv, n = TELEMETRY.coop[n0]
+        sys_ = a[sys_pos]
+        k = sys_._ctx
+        lay = np.zeros(k.coop_blocks + 2, dtype=np.int32)
+        k.call("otn_coop_layout", lay.ctypes.data)
+        m = sys_._mask.cpu().numpy()
+        rows.append((int(lay[-1]), int(np.diff(lay[:-1]).max()), int(m[:, -1].sum()), h, ms * 1e3))
+        return res
+    return wrapped
 
 
-nt._newton_device = wrapped
+nt._newton_device = wrap(nt._newton_device, 1)            # (grad_u, sys, ...)
+nt._newton_step_device = wrap(nt._newton_step_device, 1)  # (state, sys, ...)
 sol = ot.mdot(dp, 2.0 ** 5, gf)
 tot = sum(r[4] for r in rows)
 print(f"{'mode':>4} {'maxrows':>7} {'nnz':>9} {'hvps':>5} {'us':>9} {'us/hvp':>7}")

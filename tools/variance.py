@@ -26,7 +26,7 @@ for mode in ("gc-on", "gc-off"):
         ot.mdot(dp, 2.0 ** 5, 2.0 ** 16)
         torch.cuda.synchronize()
         ts.append((time.perf_counter() - t0) * 1e3)
-        cs.append(sum(a.elapsed_time(b) for (a, b, *_r) in TELEMETRY.coop))
+        cs.append(sum(ms for (ms, *_r) in TELEMETRY.coop))
         TELEMETRY.time_coop = False
     print(mode, "wall", [f"{t:.0f}" for t in ts], "coop", [f"{c:.0f}" for c in cs], flush=True)
 gc.enable()
