@@ -144,3 +144,25 @@ def test_sinkhorn_projector_path():
     assert sol.report.solver == "mdot-sinkhorn"
     np.testing.assert_allclose(sol.P.sum(axis=1), prob.r, atol=1e-12)
     assert sol.report.ops.get("sinkhorn", 0) > 0
+
+
+@pytest.mark.parametrize("spec", ["grid:32:l2sq:0", "grid:32:l1:1"])
+def test_fused_newton_step_matches_per_call_path(spec, monkeypatch):
+    """otn_newton_step (Newton + alpha = 1 trial + gated accept path, one
+    host sync) against the per-call path otn_newton -> otn_trial_cols ->
+    accept -> row LSE -> row statistics: the same kernels in the same order,
+    so the solves are bit-identical, with identical op tallies, including
+    steps that backtrack (device gate closed, host loop takes over)."""
+    from paper_2504_02067_b200.dual import DualState
+    prob = problems.workload(spec)
+    a = mdot(prob, 2.0 ** 5, 2.0 ** 14)
+    monkeypatch.setattr(DualState, "_newton_step", None)
+    b = mdot(prob, 2.0 ** 5, 2.0 ** 14)
+    np.testing.assert_array_equal(a.final_state.u, b.final_state.u)
+    np.testing.assert_array_equal(a.final_state.v, b.final_state.v)
+    np.testing.assert_array_equal(a.P, b.P)
+    assert a.report.ops == b.report.ops
+    sa = [(it.stats.newton_steps, it.stats.cg_iters, it.stats.backtracks) for it in a.iterations]
+    sb = [(it.stats.newton_steps, it.stats.cg_iters, it.stats.backtracks) for it in b.iterations]
+    assert sa == sb
+    print(spec, "backtracks", sum(x[2] for x in sa), "steps", sum(x[0] for x in sa))
