@@ -260,9 +260,10 @@ def run_ours(args, rank, world):
     return out
 
 
-# FP64-pipe instructions per plan entry in the on-the-fly pair kernel (counted
-# from the SASS of k_pair<8, DOT>: ~25 DFMA + ~17 DADD + ~8 DMUL per entry).
-PAIR_FP64_INSTR_PER_ENTRY = 50
+# FP64-pipe instructions per plan entry in the on-the-fly pair kernel at d = 3
+# (ncu smsp__inst_executed_pipe_fp64 x 32 / entries at n = 65536: 31.1 for
+# the product pass, 33.2 for the log-sum-exp pass).
+PAIR_FP64_INSTR_PER_ENTRY = 32
 
 
 def run_extras(args, rank, world, dev):
