@@ -50,6 +50,7 @@ __device__ __forceinline__ double finish(const LseArgs& a, int64_t j, double lse
 // memory, double-buffered with one barrier per step.
 constexpr int kLseRowThreads = 128;
 
+template <bool FULL>
 __global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
   __shared__ double2 s_exp[64];
   __shared__ double s_in[2][256];
@@ -57,29 +58,28 @@ __global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
   exp_tab_load(s_exp);
   const int64_t row = int64_t(blockIdx.x) * (kLseRowThreads / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  const bool valid = row < a.n;
+  const bool valid = FULL || row < a.n;
   const double* crow = a.C + (valid ? row : 0) * a.ld;
   const int64_t n = a.n;
   double m = OTN_NINF, s = 0.0;
-  // C loads run two 256-column steps ahead of the math (cur, nxt, nx2); the
-  // inner vector's next step is loaded one step ahead (raw values: the
-  // alpha * dir term is formed when staged)
+  // C loads run one 256-column step ahead of the math (cur, nxt: a deeper
+  // register prefetch costs occupancy and measured slower), as do the inner
+  // vector's (raw values: the alpha * dir term is formed when staged)
   constexpr int kIn = 256 / kLseRowThreads;
-  double2 cur[4], nxt[4], nx2[4];
+  double2 cur[4], nxt[4];
   double ib[kIn], id[kIn];
   auto load_in = [&](int64_t base) {
 #pragma unroll
     for (int q = 0; q < kIn; ++q) {
       const int64_t j = base + threadIdx.x + kLseRowThreads * q;
-      ib[q] = j < n ? __ldg(a.inner + j) : 0.0;
-      id[q] = a.inner_d && j < n ? __ldg(a.inner_d + j) : 0.0;
+      ib[q] = FULL || j < n ? __ldg(a.inner + j) : 0.0;
+      id[q] = a.inner_d && (FULL || j < n) ? __ldg(a.inner_d + j) : 0.0;
     }
   };
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int64_t j = 64 * k + 2 * lane;
-    cur[k] = valid && j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
-    nxt[k] = valid && j + 256 < n ? ld_stream2(crow + j + 256) : make_double2(0.0, 0.0);
+    cur[k] = valid && (FULL || j < n) ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
   }
   load_in(0);
   int buf = 0;
@@ -92,8 +92,10 @@ __global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
     if (base + 256 < n) load_in(base + 256);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int64_t j = base + 512 + 64 * k + 2 * lane;
-      nx2[k] = valid && j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
+      const int64_t j = base + 256 + 64 * k + 2 * lane;
+      // (FULL: the last step has no next step; j < n covers that otherwise)
+      nxt[k] = valid && (FULL ? base + 256 < n : j < n) ? ld_stream2(crow + j)
+                                                        : make_double2(0.0, 0.0);
     }
     double b[8];
 #pragma unroll
@@ -101,8 +103,8 @@ __global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
       const int jl = 64 * k + 2 * lane;
       const int64_t j = base + jl;
       const double2 in = *reinterpret_cast<const double2*>(&s_in[buf][jl]);
-      b[2 * k] = j < n ? __dadd_rn(__dmul_rn(a.ng, cur[k].x), in.x) : OTN_NINF;
-      b[2 * k + 1] = j + 1 < n ? __dadd_rn(__dmul_rn(a.ng, cur[k].y), in.y) : OTN_NINF;
+      b[2 * k] = FULL || j < n ? __dadd_rn(__dmul_rn(a.ng, cur[k].x), in.x) : OTN_NINF;
+      b[2 * k + 1] = FULL || j + 1 < n ? __dadd_rn(__dmul_rn(a.ng, cur[k].y), in.y) : OTN_NINF;
     }
     double cm = b[0];
 #pragma unroll
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
       for (int k = 0; k < 8; ++k) s = add_exp_le0(s, b[k] - m, s_exp);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) { cur[k] = nxt[k]; nxt[k] = nx2[k]; }
+    for (int k = 0; k < 4; ++k) cur[k] = nxt[k];
     buf ^= 1;
   }
   warp_lse(m, s);
@@ -352,7 +354,12 @@ cudaError_t launch_lse_rows(otn_ctx* x, const double* C, double ng, const double
                             const double* outer_d, const double* inner, const double* inner_d,
                             double alpha, int mode, double* out, const int* gate) {
   LseArgs a{C, x->n, x->ld, ng, outer, outer_d, inner, inner_d, alpha, mode, out, gate};
-  k_lse_rows<<<rows_grid(x->n, kLseRowThreads), kLseRowThreads, 0, x->stream>>>(a);
+  // full tiles (n a multiple of the 256-column step and of the rows per block):
+  // no bounds predicates in the streaming loop
+  if (x->n % 256 == 0)
+    k_lse_rows<true><<<rows_grid(x->n, kLseRowThreads), kLseRowThreads, 0, x->stream>>>(a);
+  else
+    k_lse_rows<false><<<rows_grid(x->n, kLseRowThreads), kLseRowThreads, 0, x->stream>>>(a);
   return cudaGetLastError();
 }
 
