@@ -9,10 +9,6 @@
 
 namespace otn {
 
-// One warp per row: 2-warp blocks spread the n warps evenly over the SMs
-// (256-thread blocks left some SMs a whole block behind: 3 vs 4 per SM at n=4096).
-constexpr int kRowThreads = 64;
-
 struct LseArgs {
   const double* C;
   int64_t n, ld;
@@ -208,49 +204,73 @@ __global__ void k_lse_cols_fin(LseArgs a, int slabs, const double* part) {
 // Plan: P_ij = exp_tab((ng*C_ij + v_j) + u_i), one warp per row, 16-byte stores,
 // zeros in the padding columns.  Fused K5: mu_i = (sum_j P_ij^2 icP_j)/rP_i.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kRowThreads) k_materialize(const double* __restrict__ C,
+// 4 rows (warps) per 128-thread block; each 256-column step of v and 1/cP is
+// staged once per block in shared memory (double-buffered, loaded one step
+// ahead), so a row's registers hold only its C prefetch.  FULL: n is a
+// multiple of the step, no bounds predicates in the loop.
+constexpr int kMatThreads = 128;
+
+template <bool FULL>
+__global__ void __launch_bounds__(kMatThreads) k_materialize(const double* __restrict__ C,
     int64_t n, int64_t ld, double ng, const double* __restrict__ u, const double* __restrict__ v,
     double* __restrict__ P, const double* __restrict__ icP, const double* __restrict__ rP,
     double* __restrict__ mu, int* __restrict__ flag, uint64_t* __restrict__ mask) {
   __shared__ double2 s_exp[64];
+  __shared__ double s_v[2][256], s_ic[2][256];
   exp_tab_load(s_exp);
-  __syncthreads();
-  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t row = int64_t(blockIdx.x) * (kMatThreads / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (row >= n) return;
-  const double* crow = C + row * ld;
-  double* prow = P + row * ld;
-  const double ui = __ldg(u + row);
+  const bool valid = FULL || row < n;               // every thread joins the block barriers
+  const double* crow = C + (valid ? row : 0) * ld;
+  double* prow = P + (valid ? row : 0) * ld;
+  const double ui = valid ? __ldg(u + row) : 0.0;
   const int64_t mw = OTN_MASK_WORDS(ld);
   double acc = 0.0, mx = OTN_NINF;
   uint64_t bits = 0;
   int nnz = 0;
-  // one 256-column step per iteration, its loads issued one step ahead
-  double2 cc[4], cn[4];
-  double vc[8], vn[8], ic[8], inx[8];
-  auto load = [&](int64_t base, double2 (&c)[4], double (&vv)[8], double (&ii)[8]) {
+  constexpr int kIn = 256 / kMatThreads;
+  double vb[kIn], ib[kIn];
+  auto load_in = [&](int64_t base) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t j = base + 64 * k + 2 * lane;
-      c[k] = j < n ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
-      vv[2 * k] = j < n ? __ldg(v + j) : 0.0;
-      vv[2 * k + 1] = j + 1 < n ? __ldg(v + j + 1) : 0.0;
-      ii[2 * k] = icP && j < n ? __ldg(icP + j) : 0.0;
-      ii[2 * k + 1] = icP && j + 1 < n ? __ldg(icP + j + 1) : 0.0;
+    for (int q = 0; q < kIn; ++q) {
+      const int64_t j = base + threadIdx.x + kMatThreads * q;
+      vb[q] = FULL || j < n ? __ldg(v + j) : 0.0;
+      ib[q] = icP && (FULL || j < n) ? __ldg(icP + j) : 0.0;
     }
   };
-  load(0, cc, vc, ic);
+  double2 cur[4], nxt[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t j = 64 * k + 2 * lane;
+    cur[k] = valid && (FULL || j < n) ? ld_stream2(crow + j) : make_double2(0.0, 0.0);
+  }
+  load_in(0);
+  int buf = 0;
   for (int64_t base = 0; base < ld; base += 256) {
-    if (base + 256 < ld) load(base + 256, cn, vn, inx);
+#pragma unroll
+    for (int q = 0; q < kIn; ++q) {
+      s_v[buf][threadIdx.x + kMatThreads * q] = vb[q];
+      s_ic[buf][threadIdx.x + kMatThreads * q] = ib[q];
+    }
+    __syncthreads();                                 // also publishes s_exp on the first step
+    if (base + 256 < ld) load_in(base + 256);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int64_t j = base + 64 * k + 2 * lane;
+      const int64_t j = base + 256 + 64 * k + 2 * lane;
+      nxt[k] = valid && (FULL ? base + 256 < n : j < n) ? ld_stream2(crow + j)
+                                                        : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int jl = 64 * k + 2 * lane;
+      const int64_t j = base + jl;
       bool nz = false;
-      if (j < ld) {
+      if (valid && (FULL || j < ld)) {
+        const double2 vv = *reinterpret_cast<const double2*>(&s_v[buf][jl]);
         double e0 = OTN_NINF, e1 = OTN_NINF;
-        if (j < n) {
-          e0 = __dadd_rn(__dadd_rn(__dmul_rn(ng, cc[k].x), vc[2 * k]), ui);
-          if (j + 1 < n) e1 = __dadd_rn(__dadd_rn(__dmul_rn(ng, cc[k].y), vc[2 * k + 1]), ui);
+        if (FULL || j < n) {
+          e0 = __dadd_rn(__dadd_rn(__dmul_rn(ng, cur[k].x), vv.x), ui);
+          if (FULL || j + 1 < n) e1 = __dadd_rn(__dadd_rn(__dmul_rn(ng, cur[k].y), vv.y), ui);
         }
         mx = fmax(mx, fmax(e0, e1));
         const double p0 = exp_tab(e0, s_exp), p1 = exp_tab(e1, s_exp);
@@ -258,22 +278,23 @@ __global__ void __launch_bounds__(kRowThreads) k_materialize(const double* __res
         nz = (p0 != 0.0) || (p1 != 0.0);
         nnz += int(p0 != 0.0) + int(p1 != 0.0);
         if (icP) {
-          if (j < n) acc = fma(__dmul_rn(p0, p0), ic[2 * k], acc);
-          if (j + 1 < n) acc = fma(__dmul_rn(p1, p1), ic[2 * k + 1], acc);
+          const double2 ii = *reinterpret_cast<const double2*>(&s_ic[buf][jl]);
+          if (FULL || j < n) acc = fma(__dmul_rn(p0, p0), ii.x, acc);
+          if (FULL || j + 1 < n) acc = fma(__dmul_rn(p1, p1), ii.y, acc);
         }
       }
       // segment (64 columns = 512 B) occupancy bit for the HVP's zero skipping
       if (__ballot_sync(0xffffffffu, nz)) bits |= 1ull << (((base >> 6) + k) & 63);
     }
-    if (mask && (((base + 256) % kSegWordCols) == 0 || base + 256 >= ld)) {
+    if (mask && valid && (((base + 256) % kSegWordCols) == 0 || base + 256 >= ld)) {
       if (lane == 0) mask[row * mw + base / kSegWordCols] = bits;
       bits = 0;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) cc[k] = cn[k];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) { vc[k] = vn[k]; ic[k] = inx[k]; }
+    for (int k = 0; k < 4; ++k) cur[k] = nxt[k];
+    buf ^= 1;
   }
+  if (!valid) return;
   mx = warp_max(mx);
   if (icP) acc = warp_sum(acc);
   if (mask) {
@@ -378,8 +399,13 @@ cudaError_t launch_lse_cols(otn_ctx* x, const double* C, double ng, const double
 cudaError_t launch_materialize(otn_ctx* x, const double* C, double ng, const double* u,
                                const double* v, double* P, const double* icP, const double* rP,
                                double* mu, int* flag, uint64_t* mask) {
-  k_materialize<<<rows_grid(x->n, kRowThreads), kRowThreads, 0, x->stream>>>(C, x->n, x->ld, ng, u, v, P, icP,
-                                                                 rP, mu, flag, mask);
+  const unsigned grid = rows_grid(x->n, kMatThreads);
+  if (x->n == x->ld && x->n % 256 == 0)
+    k_materialize<true><<<grid, kMatThreads, 0, x->stream>>>(C, x->n, x->ld, ng, u, v, P, icP, rP,
+                                                             mu, flag, mask);
+  else
+    k_materialize<false><<<grid, kMatThreads, 0, x->stream>>>(C, x->n, x->ld, ng, u, v, P, icP, rP,
+                                                              mu, flag, mask);
   return cudaGetLastError();
 }
 
