@@ -279,6 +279,12 @@ int otn_vec(otn_ctx* ctx, int op, double s, const double* a, const double* b, co
             const double* d, double* out);
 int otn_reduce(otn_ctx* ctx, int op, const double* a, const double* b, const double* c,
                const double* d, double* host_out, int* host_flags);
+/* As otn_reduce without the host synchronization: the two results are copied
+ * stream-ordered into host_out, which must be page-locked; they are valid
+ * once the stream has passed this point (record an event after the call).
+ * For read-backs the control flow does not wait on (per-stage telemetry). */
+int otn_reduce_async(otn_ctx* ctx, int op, const double* a, const double* b, const double* c,
+                     const double* d, double* host_out_pinned);
 /* Round P onto U(r, c) in place and return host_out = {<P, C>, deficit}
  * (driver.py:178-208 round_plan + driver.py:306-310 vdot).  C may be NULL
  * (primal cost skipped).  host_flags: 1 = negative entry (DomainError),

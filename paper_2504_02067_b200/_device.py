@@ -58,7 +58,7 @@ LAUNCHES = {
     "otn_newton": 2, "otn_probe": 2,
     # newton (2) + gate + trial (1 | 2) + mass + gate + u, v, lc + row LSE + grad + row stats
     "otn_newton_step": 13,
-    "otn_vec": 1, "otn_reduce": 1, "otn_round_plan": 10, "otn_pc_pass": 1,
+    "otn_vec": 1, "otn_reduce": 1, "otn_reduce_async": 1, "otn_round_plan": 10, "otn_pc_pass": 1,
     "otn_vec_n": 1, "otn_reduce_n": 1,
 }
 

@@ -577,6 +577,19 @@ int otn_vec(otn_ctx* x, int op, double s, const double* a, const double* b, cons
   return OTN_OK;
 }
 
+int otn_reduce_async(otn_ctx* x, int op, const double* a, const double* b, const double* c,
+                     const double* d, double* host_out) {
+  OTN_REQUIRE(x && a && host_out, "otn_reduce_async: NULL argument");
+  OTN_REQUIRE(op >= OTN_RED_ROW_STATS && op <= OTN_RED_L1_DOT, "otn_reduce_async: bad op");
+  // own scalar slot (40..41) and flag word (9): later reductions cannot
+  // overwrite the result before the copy runs (stream order), nor race it
+  OTN_CUDA(otn::launch_reduce(x, op, x->n, a, b, c, d, x->scal + 40, x->flags + 9),
+           "otn_reduce_async");
+  OTN_CUDA(cudaMemcpyAsync(host_out, x->scal + 40, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                           x->stream), "otn_reduce_async: copy");
+  return OTN_OK;
+}
+
 int otn_reduce(otn_ctx* x, int op, const double* a, const double* b, const double* c,
                const double* d, double* host_out, int* host_flags) {
   OTN_REQUIRE(x && a && host_out, "otn_reduce: NULL argument");

@@ -39,6 +39,21 @@ def device_cost(problem, device=None):
     return dc
 
 
+class DeferredScalar:
+    """A device reduction result in flight: value() = out[0] + out[1] once the
+    stream has reached the copy (telemetry the control flow does not branch on)."""
+
+    __slots__ = ("_host", "_event")
+
+    def __init__(self, host, event):
+        self._host, self._event = host, event
+
+    def value(self):
+        self._event.synchronize()
+        h = self._host.numpy()
+        return float(h[0] + h[1])
+
+
 class DualState:
     """Single-owner mutable dual state at one temperature (dual.py:22-46)."""
 
@@ -247,6 +262,18 @@ class DualState:
         self._ctx.call("otn_reduce", _lib.RED_GRAD_L1, vptr(self._lr_dev()), vptr(self._r),
                        vptr(self._lc_dev()), vptr(self._c), out, None)
         return float(out[0] + out[1])
+
+    def _grad_norm_l1_deferred(self):
+        """grad_norm_l1 without waiting for it: the reduction is enqueued and its
+        result read back stream-ordered into page-locked memory; the returned
+        object's value() waits only if the stream has not passed it yet."""
+        t = torch()
+        host = t.empty(2, dtype=t.float64, pin_memory=True)
+        self._ctx.call("otn_reduce_async", _lib.RED_GRAD_L1, vptr(self._lr_dev()), vptr(self._r),
+                       vptr(self._lc_dev()), vptr(self._c), ctypes.c_void_p(host.data_ptr()))
+        ev = t.cuda.Event()
+        ev.record(t.cuda.current_stream(self._ctx.device))
+        return DeferredScalar(host, ev)
 
     def dual_value(self):
         """sum(P) - 1 - <u, r> - <v, c> (dual.py:150-153)."""
