@@ -41,15 +41,17 @@ def device_cost(problem, device=None):
 
 class DeferredScalar:
     """A device reduction result in flight: value() = out[0] + out[1] once the
-    stream has reached the copy (telemetry the control flow does not branch on)."""
+    stream has passed the copy (telemetry the control flow does not branch on).
+    A fresh 64-slot block is allocated when one fills, so a slot is never
+    reused while a value in it is pending."""
 
-    __slots__ = ("_host", "_event")
+    __slots__ = ("_host", "_stream")
 
-    def __init__(self, host, event):
-        self._host, self._event = host, event
+    def __init__(self, host, stream):
+        self._host, self._stream = host, stream
 
     def value(self):
-        self._event.synchronize()
+        self._stream.synchronize()
         h = self._host.numpy()
         return float(h[0] + h[1])
 
@@ -265,15 +267,18 @@ class DualState:
 
     def _grad_norm_l1_deferred(self):
         """grad_norm_l1 without waiting for it: the reduction is enqueued and its
-        result read back stream-ordered into page-locked memory; the returned
-        object's value() waits only if the stream has not passed it yet."""
+        result read back stream-ordered into a page-locked slot; value() waits
+        for the stream only if it has not passed the copy yet."""
         t = torch()
-        host = t.empty(2, dtype=t.float64, pin_memory=True)
+        slots = getattr(self, "_gn_slots", None)
+        if slots is None or self._gn_next == slots.shape[0]:
+            slots = self._gn_slots = t.empty((64, 2), dtype=t.float64, pin_memory=True)
+            self._gn_next = 0
+        host = slots[self._gn_next]
+        self._gn_next += 1
         self._ctx.call("otn_reduce_async", _lib.RED_GRAD_L1, vptr(self._lr_dev()), vptr(self._r),
                        vptr(self._lc_dev()), vptr(self._c), ctypes.c_void_p(host.data_ptr()))
-        ev = t.cuda.Event()
-        ev.record(t.cuda.current_stream(self._ctx.device))
-        return DeferredScalar(host, ev)
+        return DeferredScalar(host, t.cuda.current_stream(self._ctx.device))
 
     def dual_value(self):
         """sum(P) - 1 - <u, r> - <v, c> (dual.py:150-153)."""
@@ -443,8 +448,19 @@ class DualState:
         return self._ctx.download(buf)
 
     def _snapshot(self):
-        """Device copy of (u, v) for the annealing driver's extrapolation."""
-        return self._u.clone(), self._v.clone()
+        """Device copy of (u, v) for the annealing driver's extrapolation.  The
+        driver holds at most the previous and the current snapshot, so two
+        buffer pairs alternate (stream-ordered copies, no allocation)."""
+        k = self._ctx
+        pairs = getattr(self, "_snap_bufs", None)
+        if pairs is None:
+            pairs = self._snap_bufs = ((k.vec(), k.vec()), (k.vec(), k.vec()))
+            self._snap_next = 0
+        u, v = pairs[self._snap_next]
+        self._snap_next ^= 1
+        k.copy(u, self._u)
+        k.copy(v, self._v)
+        return u, v
 
     def _extrapolate(self, step, z_cur, z_prev):
         """(u, v) = z + step * (z - z_prev)  (driver.py:170-175)."""
