@@ -1,0 +1,22 @@
+import ctypes, sys
+sys.path.insert(0, '.')
+import numpy as np, torch
+import paper_2504_02067_b200 as ot
+from paper_2504_02067_b200 import _lib
+lib = _lib.load()
+p = ot.workload("grid:64:l2sq:0")
+dp = ot.Problem(C=torch.from_numpy(p.C).cuda(), r=p.r, c=p.c)
+ot.mdot(dp, 2.0**5, 2.0**16)
+buf = (ctypes.c_ulonglong * 48)()
+lib.otn_dbg_seg(buf)
+sol = ot.mdot(dp, 2.0**5, 2.0**16)
+lib.otn_dbg_seg(buf)
+a = np.frombuffer(buf, dtype=np.uint64).reshape(4, 12).astype(float)
+names = ["loop top", "a2_sums", "rz reduce_end", "a2_tail", "pq reduce_begin", "phase B",
+         "pq reduce_end", "vector updates", "stage_x", "phase A", "rz reduce_begin", "-"]
+hv = {0: 414, 2: 2025, 3: 658}
+for m in (0, 2, 3):
+    tot = a[m].sum()
+    print(f"mode {m}: total {tot/1.965e3/1e3:.2f} ms  ({tot/1.965e3/hv[m]:.2f} us per hvp approx)")
+    for i, nm in enumerate(names[:11]):
+        print(f"   {nm:18s} {a[m][i]/1.965e3/hv[m]:7.2f} us/it")
