@@ -1,3 +1,5 @@
+"""Per-segment cycle breakdown of the CG iteration per plan mode (CTA 0):
+    python tools/make_seg_build.py && OTN_LIB_AB=build/ab/libotn_seg.so python tools/seg_run.py"""
 import ctypes, sys
 sys.path.insert(0, '.')
 import numpy as np, torch
