@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
         }
         if (m[r] != OTN_NINF) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) s[r] = add_exp_le0(s[r], e[q] - m[r], s_exp);
+          for (int q = 0; q < 8; ++q) s[r] += exp_tab(e[q] - m[r], s_exp);
         }
       }
     } else {
