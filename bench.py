@@ -266,6 +266,46 @@ def run_ours(args, rank, world):
 PAIR_FP64_INSTR_PER_ENTRY = 32
 
 
+def fused_px(dev, reps=200):
+    """BASELINE's "fused P.x GB/s": steady-state time of one HVP (P^T x, A2,
+    P w: 16 n^2 algorithmic bytes) inside the persistent kernel, repeated
+    `reps` times in one launch on the D2 L2^2 plan of the first stage (dense,
+    gamma 2^5) and of the last (gamma 2^16, ~450 K nonzeros).  P (134 MB) is
+    about the L2 size, so part of the stream is served from L2."""
+    import torch
+
+    import paper_2504_02067_b200 as ot
+    from paper_2504_02067_b200._device import vptr
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    p = ot.workload("grid:64:l2sq:0")
+    dp = ot.Problem(C=torch.from_numpy(p.C).to(dev), r=p.r, c=p.c)
+    res = {}
+    for key, gf in (("dense_gamma_2^5", 2.0 ** 5), ("sparse_gamma_2^16", 2.0 ** 16)):
+        st = ot.mdot(dp, 2.0 ** 5, gf).final_state
+        s = ot.DiscountedSystem.from_state(st)
+        k = s._ctx
+        x = torch.randn(k.ld, dtype=torch.float64, device=dev)
+        out = k.vec()
+
+        def go(n):
+            k.call("otn_probe", vptr(s._P), vptr(s._mask), vptr(s._cP), vptr(s._rP), vptr(x),
+                   vptr(out), 5, n)
+        go(reps)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        go(reps)
+        e1.record()
+        e1.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / reps
+        alg = 16.0 * p.n * p.n
+        res[key] = {"hvp_us": us, "alg_bytes": alg, "gbps": alg / (us * 1e-6) / 1e9,
+                    "frac_of_hbm_peak": alg / (us * 1e-6) / 1e9 / peak}
+    res["peak_gbps"] = peak
+    return res
+
+
 def run_extras(args, rank, world, dev):
     """The other BASELINE configurations, one timed solve each (after a warm-up):
     D1 (n=1024 2-D points, fixed gamma), D3 (n=4096 784-d pixel sets, stored C),
@@ -300,6 +340,7 @@ def run_extras(args, rank, world, dev):
                                "stages": len(sol.iterations),
                                "cg": sum(i.stats.cg_iters for i in sol.iterations),
                                "true_marginal_err": st.grad_norm_l1()}
+            extras["fused_px"] = fused_px(dev)
         n4 = args.d4_n
         pc = ot.points_problem(n4, 3, 0)
         comm = Comm()
