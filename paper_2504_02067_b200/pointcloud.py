@@ -24,12 +24,11 @@ The state class mirrors the private hooks ``project()`` and ``mdot()`` use on
 from __future__ import annotations
 
 import ctypes
-import math
 
 import numpy as np
 
 from . import _lib, opcount
-from ._device import TELEMETRY, Context, is_tensor, torch, vptr
+from ._device import TELEMETRY, Context, torch, vptr
 from .errors import (
     ConditioningError,
     DegenerateInputError,

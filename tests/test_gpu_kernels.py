@@ -190,7 +190,6 @@ def test_exp_fast_accuracy(op):
     range, exact 0 / inf / NaN at the ends.  VEC_EXP runs exp_tab (the
     table-driven exp of every LSE / plan / pair entry); VEC_GRAD with b = 0
     runs exp_fast (the polynomial one used for O(n) work and LSE merges)."""
-    import torch
     from paper_2504_02067_b200 import _lib
     from paper_2504_02067_b200._device import Context, require_cuda, vptr
     rng = np.random.default_rng(0)
