@@ -686,7 +686,20 @@ __device__ void phase_b_sparse(void* sg, const double* w, int64_t r0, int64_t r1
   const int ulo = s_win_lo[0], W = s_win_hi[0] - ulo;
   double* ws = sp.xs - ulo;                         // ws[j] for window columns j
   __syncthreads();
-  for (int d = t; d < W; d += NT) sp.xs[d] = __ldcg(w + ulo + d);
+  {
+    // all of this thread's window loads in flight at once (W <= TILE = 8 NT)
+    double wv[TILE / NT];
+#pragma unroll
+    for (int u = 0; u < TILE / NT; ++u) {
+      const int d = t + u * NT;
+      wv[u] = d < W ? __ldcg(w + ulo + d) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < TILE / NT; ++u) {
+      const int d = t + u * NT;
+      if (d < W) sp.xs[d] = wv[u];
+    }
+  }
   __syncthreads();
   for (int r = warp; r < rows; r += NW) {
     double dot = 0.0;
