@@ -625,7 +625,9 @@ __device__ void phase_a_sparse(void* sg, int64_t r0, int64_t r1, double* wrow, S
     // entries are loaded 8 at a time regardless of column boundaries (columns
     // are short: a load per column would expose the full L2 / shared-memory
     // latency), then consumed in order with the column bookkeeping in registers
-    int m = s_m0[t], mend = cptr[m + 1];
+    // the current column's end and window column are kept in registers, the
+    // next ones loaded as soon as a column closes (the store never waits)
+    int m = s_m0[t], mend = cptr[m + 1], mcol = ccol[m];
     bool begun = cptr[m] < kb;                      // column started in an earlier thread
     double acc = 0.0;
     const int S = s_split;
@@ -654,17 +656,18 @@ __device__ void phase_a_sparse(void* sg, int64_t r0, int64_t r1, double* wrow, S
         if (k >= ke) break;
         if (k == mend) {                            // column m ended inside this thread
           if (begun) head[t] = acc;
-          else wrow[ulo + ccol[m]] = acc;
+          else wrow[ulo + mcol] = acc;
           begun = false;
           acc = 0.0;
           ++m;
           mend = cptr[m + 1];
+          mcol = ccol[m];
         }
         acc = fma(pv[u], xv[u], acc);
       }
     }
     if (begun) head[t] = acc;                       // piece of a column begun earlier
-    else if (mend <= ke) wrow[ulo + ccol[m]] = acc; // whole column inside this thread
+    else if (mend <= ke) wrow[ulo + mcol] = acc;    // whole column inside this thread
     else { tail = acc; tail_m = m; }                // column continues in later threads
   }
   __syncthreads();
