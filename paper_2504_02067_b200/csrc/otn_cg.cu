@@ -838,11 +838,13 @@ __device__ __noinline__ void a2_sums(const CoopArgs& a, Smem& sh) {
   sh.a2[warp][lane] = acc;
 }
 
-// After a2_sums and a barrier: out_j = w_j / cP_j (kind 0) with
-// w = sum + beta * wprev (if wprev), w kept in wkeep; returns w_j * out_j
-// for warp 0's lanes.
-__device__ __forceinline__ double a2_tail(const CoopArgs& a, double* out, Smem& sh,
-                                          const double* wprev, double beta, double* wkeep) {
+// After a2_sums and a barrier: out_j = w_j / cP_j with w = sum + beta * wreg,
+// for warp 0's lanes (column j = 32 * blockIdx.x + lane).  wreg holds the
+// previous w_j in a register (the same thread formed it last iteration) and
+// receives the new one, which is also kept in a.q; cPj is 1/cP's divisor,
+// loaded once per launch.  Returns w_j * out_j.  Same arithmetic as phase_a2.
+__device__ __forceinline__ double a2_tail(const CoopArgs& a, double* out, Smem& sh, double beta,
+                                          double& wreg, double cPj) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t s = blockIdx.x;
   double wq = 0.0;
@@ -851,11 +853,12 @@ __device__ __forceinline__ double a2_tail(const CoopArgs& a, double* out, Smem& 
     double tot = 0.0;
 #pragma unroll 8
     for (int w = 0; w < NW; ++w) tot += sh.a2[w][lane];
-    if (wprev) tot = __dadd_rn(tot, __dmul_rn(beta, __ldcg(wprev + j)));
-    if (wkeep) wkeep[j] = tot;
+    tot = __dadd_rn(tot, __dmul_rn(beta, wreg));
+    a.q[j] = tot;
+    wreg = tot;
     double val = 0.0;
     if (j < a.n) {
-      val = __ddiv_rn(tot, __ldg(a.cP + j));
+      val = __ddiv_rn(tot, cPj);
       wq = fma(tot, val, wq);
     }
     out[j] = val;
@@ -1072,6 +1075,12 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
   double beta = 0.0;
   bool fresh = true;                                // no previous direction yet
   const bool split = mv && a2_single_slice(a);      // overlap the r.z reduction with A2's loads
+  // split A2: warp 0's lanes own column slice_j of P^T p; its previous value
+  // and cP stay in registers
+  const int64_t slice_j = int64_t(blockIdx.x) * 32 + (threadIdx.x & 31);
+  const bool slice_lane = (threadIdx.x >> 5) == 0 && slice_j < a.ld;
+  double wreg = 0.0;
+  const double cPj = split && slice_lane && slice_j < a.n ? __ldg(a.cP + slice_j) : 1.0;
   bool pending = false;                             // an r.z reduction begun, not finished
   double nz[2] = {0.0, 0.0};
   for (int64_t k = 1; k <= max_iters; ++k) {
@@ -1090,7 +1099,7 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
       p = __dadd_rn(z, __dmul_rn(beta, p));
       rz = nz[1];
       ++nh;
-      wq = a2_tail(a, a.wc, sh, fresh ? nullptr : a.q, beta, a.q);
+      wq = a2_tail(a, a.wc, sh, beta, wreg, cPj);
     }
     q = __dmul_rn(rPi, p);
     double pq;
@@ -1098,6 +1107,7 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
       if (!split || fresh) {
         ++nh;
         wq = phase_a2(a, 0, a.wc, sh, fresh ? nullptr : a.q, beta, a.q);
+        if (split && slice_lane) wreg = __ldcg(a.q + slice_j);   // just written by this thread
       }
       double sums[2] = {fma(p, q, 0.0), wq};
       grid_reduce_begin<2>(grid, sums, a.red, slot, sh);
