@@ -616,8 +616,10 @@ __device__ void phase_a_sparse(void* sg, int64_t r0, int64_t r1, double* wrow, S
   double* head = &sh.bp[0][0];                      // per-thread piece of a column begun earlier
   const double* xs = sh.xs;
   const int ulo = s_win_lo[0];
-  head[t] = 0.0;
-  __syncthreads();
+  // (no initialization of head: every head[u] the joins below read is written
+  // in this call — a thread whose range starts inside a column always ends
+  // with `begun` set or closes that column; the caller's stage_x barrier
+  // orders this call after the previous readers)
   const int kb = s_kb[t], ke = s_kb[t + 1];
   double tail = 0.0;
   int tail_m = -1;
