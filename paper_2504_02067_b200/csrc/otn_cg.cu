@@ -1344,10 +1344,12 @@ __global__ void __launch_bounds__(kPartThreads) k_partition(const uint64_t* mask
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   int mode = kPlanRing;
   bool sparse = false;
+  int64_t s_nz = 0;                                  // nonzeros of the plan (all threads)
   if (mask) {
     int64_t nz = 0;
     for (int64_t i = t; i < n; i += kPartThreads) nz += int64_t(__ldg(mask + i * mw + mw - 1));
     nz = block_sum_part<int64_t>(nz, s_buf);
+    s_nz = nz;
     const int64_t cap = sg_ok ? kSparseGCap : kSparseCap;
     // compressed rows pay 10 B per nonzero per pass (value + column) against
     // 8 B per span column: only below half density
@@ -1401,7 +1403,11 @@ __global__ void __launch_bounds__(kPartThreads) k_partition(const uint64_t* mask
     }
     const int no_smem = block_sum_part<int>(bad_smem, s_ibuf);
     const int no_glob = block_sum_part<int>(bad_glob, s_ibuf);
-    sparse = no_smem == 0 || no_glob == 0;
+    // the global-memory CSR/CSC pays 20 B per nonzero per HVP through L2
+    // (CSR for phase B, CSC for phase A): above ~25% density the dense ring
+    // is faster (measured: 33% density 63 us vs ~34 us per HVP)
+    const bool glob_ok = no_glob == 0 && s_nz * 4 <= int64_t(n) * ld;
+    sparse = no_smem == 0 || glob_ok;
     if (sparse) mode = no_smem == 0 ? kPlanSparse : kPlanSparseG;
   }
   __syncthreads();
