@@ -239,7 +239,8 @@ def _sparse_plan(n, per_row, seed, heavy=0):
 
 @pytest.mark.parametrize("n,per_row,heavy,mode", [
     (64, 3, 0, 2), (300, 8, 0, 2), (1024, 20, 5, 2), (4096, 12, 9, 2),
-    (1024, 1024, 0, 0), (2048, 1400, 0, 3), (2048, 2048, 0, 0), (4096, 4096, 0, 0)])
+    (1024, 1024, 0, 0), (4096, 600, 0, 3), (2048, 1400, 0, 0), (2048, 2048, 0, 0),
+    (4096, 4096, 0, 0)])
 def test_hvp_plan_modes(n, per_row, heavy, mode):
     """Every plan mode (0 streamed ring, 2 sparse shared-memory rows, 3 sparse
     global-memory rows; mode 1 is retired) against numpy on the same plan; the
