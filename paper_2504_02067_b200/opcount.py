@@ -10,7 +10,6 @@ bookkeeping only; device kernels never touch it.
 from __future__ import annotations
 
 import os
-from contextlib import contextmanager
 
 
 class OpCounter:
@@ -34,13 +33,25 @@ class OpCounter:
     def snapshot(self):
         return dict(self.by_category)
 
-    @contextmanager
     def category(self, name):
-        self._stack.append(name)
-        try:
-            yield
-        finally:
-            self._stack.pop()
+        return _Category(self._stack, name)
+
+
+class _Category:
+    """`with COUNTER.category(name):` — a plain context manager (the driver
+    enters several per Newton step, on the host's critical path)."""
+
+    __slots__ = ("_stack", "_name")
+
+    def __init__(self, stack, name):
+        self._stack, self._name = stack, name
+
+    def __enter__(self):
+        self._stack.append(self._name)
+
+    def __exit__(self, *exc):
+        self._stack.pop()
+        return False
 
 
 COUNTER = OpCounter()
