@@ -273,12 +273,22 @@ def _newton_step_device(state, sys, grad_u, eta, rho0, zero_init, max_cg_iters, 
     out = (ctypes.c_double * 5)()
     fl = ctypes.c_int(0)
     timed = k.coop_timing()
-    ccols, sym = state._dc.col_args()
-    k.call("otn_newton_step", vptr(sys._P), vptr(sys._mask), vptr(sys._rP), vptr(sys._cP),
-           vptr(sys._mu()), vptr(grad_u), float(eta), float(rho0), int(bool(zero_init)),
-           int(max_cg_iters), vptr(d_u), vptr(d_v), state._dc.ptr(), ccols, sym, state._ng,
-           vptr(state._u), vptr(state._v), vptr(state._r), vptr(state._log_c),
-           vptr(state._trial_vec), vptr(state._lc), vptr(state._lr), vptr(state._g),
+    # every buffer is a persistent one of the state (its plan / system buffers,
+    # direction buffers, potentials, caches): their pointers are built once
+    key = (sys._P.data_ptr(), sys._rP.data_ptr(), d_u.data_ptr(), d_v.data_ptr(),
+           grad_u.data_ptr())
+    cached = getattr(state, "_nstep_ptrs", None)
+    if cached is None or cached[0] != key:
+        ccols, sym = state._dc.col_args()
+        head = (vptr(sys._P), vptr(sys._mask), vptr(sys._rP), vptr(sys._cP), vptr(sys._mu()),
+                vptr(grad_u))
+        mid = (vptr(d_u), vptr(d_v), state._dc.ptr(), ccols, sym)
+        tail = (vptr(state._u), vptr(state._v), vptr(state._r), vptr(state._log_c),
+                vptr(state._trial_vec), vptr(state._lc), vptr(state._lr), vptr(state._g))
+        cached = state._nstep_ptrs = (key, head, mid, tail)
+    _, head, mid, tail = cached
+    k.call("otn_newton_step", *head, float(eta), float(rho0), int(bool(zero_init)),
+           int(max_cg_iters), *mid, state._ng, *tail,
            float(armijo_c1), float(slope_floor), ctypes.byref(res), out, ctypes.byref(fl))
     if timed:
         TELEMETRY.coop.append((k.coop_ms(), int(res.hvps), 1, k.n))
