@@ -1034,10 +1034,13 @@ struct PcgOut {
 // Pipelined matvec: the phase-A partials of the next direction are formed
 // from z BEFORE the r.z reduction, and phase A2 combines them as
 // P^T p_new = P^T z + beta * P^T p (the previous direction's column sums are
-// kept in a.q), so the r.z barrier doubles as the HVP's partials barrier:
-// 3 grid barriers per CG iteration instead of 4.  The CG recurrences (x, r,
-// z, p, alpha, beta and the stopping tests) are the reference's, operation
-// for operation; only the column sums of P^T p are formed by linearity.
+// kept in a.q, and for the single-slice split in a register of warp 0), so
+// the r.z barrier doubles as the HVP's partials barrier; p.q is reduced with
+// the A2 -> phase B barrier (see the loop): 2 grid barriers per CG iteration
+// instead of 4, both reductions split around independent work.  The CG
+// recurrences (x, r, z, p, alpha, beta and the stopping tests) are the
+// reference's, operation for operation; only the column sums of P^T p and
+// the matvec part of p.q are formed by linearity.
 __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, double rPi, double rho,
                       const double* bvec, double tol, double& x, bool has_x0, int64_t max_iters,
                       int64_t r0, int64_t r1, int& slot, Smem& sh, int64_t& nh) {
