@@ -56,8 +56,9 @@ LAUNCHES = {
     "otn_materialize": 1, "otn_plan_mask": 1, "otn_system_prep": 1, "otn_square_matvec": 1,
     "otn_matvec": 2, "otn_rmatvec": 2, "otn_apply_F": 2, "otn_apply_pc": 2, "otn_pcg": 2,
     "otn_newton": 2, "otn_probe": 2,
-    # newton (2) + gate + trial (1 | 2) + mass + gate + u, v, lc + row LSE + grad + row stats
-    "otn_newton_step": 13,
+    # newton (2) + gate + trial (1 | 2) + mass + gate + accept (u, v, lc) + row LSE
+    # + row stats with the gradient
+    "otn_newton_step": 10,
     "otn_vec": 1, "otn_reduce": 1, "otn_reduce_async": 1, "otn_round_plan": 10, "otn_pc_pass": 1,
     "otn_vec_n": 1, "otn_reduce_n": 1,
 }

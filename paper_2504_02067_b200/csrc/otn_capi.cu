@@ -480,19 +480,13 @@ int otn_newton_step(otn_ctx* x, const double* P, const uint64_t* m, const double
   OTN_CUDA(otn::launch_step_gate(x, 1, x->dres, x->scal + 32, slope_floor, armijo_c1, gates),
            "otn_newton_step: armijo");
   const int* acc = gates + 1;
-  OTN_CUDA(otn::launch_vec(x, OTN_VEC_AXPY, n, 1.0, u, d_u, nullptr, nullptr, u, acc),
-           "otn_newton_step: u");
-  OTN_CUDA(otn::launch_vec(x, OTN_VEC_STEP_V, n, 1.0, v, d_v, log_c, trial, v, acc),
-           "otn_newton_step: v");
-  OTN_CUDA(otn::launch_vec(x, OTN_VEC_COPY, x->ld, 0.0, log_c, nullptr, nullptr, nullptr, lc, acc),
-           "otn_newton_step: lc");
+  OTN_CUDA(otn::launch_accept(x, 1.0, u, d_u, v, d_v, log_c, trial, lc, acc),
+           "otn_newton_step: accept");
   OTN_CUDA(otn::launch_lse_rows(x, C, ng, u, nullptr, v, nullptr, 0.0, 0, lr, acc),
            "otn_newton_step: rows");
-  OTN_CUDA(otn::launch_vec(x, OTN_VEC_GRAD, n, 0.0, lr, r, nullptr, nullptr, grad, acc),
-           "otn_newton_step: grad");
-  OTN_CUDA(otn::launch_reduce(x, OTN_RED_ROW_STATS, n, lr, r, nullptr, nullptr, x->scal + 33,
+  OTN_CUDA(otn::launch_reduce(x, otn::kRedRowStatsGrad, n, lr, r, grad, nullptr, x->scal + 33,
                               x->flags + 8, acc),
-           "otn_newton_step: row stats");
+           "otn_newton_step: row stats + gradient");
   OTN_CUDA(cudaMemcpyAsync(x->h_scal + 32, x->scal + 32, 3 * sizeof(double),
                            cudaMemcpyDeviceToHost, x->stream), "otn_newton_step: copy");
   OTN_CUDA(cudaMemcpyAsync(x->h_flags + 6, x->flags + 6, 3 * sizeof(int), cudaMemcpyDeviceToHost,

@@ -117,6 +117,13 @@ cudaError_t launch_reduce(otn_ctx* x, int op, int64_t n, const double* a, const 
 // Newton-step gates (otn_newton_step): stage 0 -> flags[0] = (status OK and
 // slope > 0), flags[2] = 0; stage 1 -> flags[1] = flags[0] and the Armijo test
 // passes at alpha = 1 (mass = *mass).
+// The accept path's vector updates in one launch (projector.py:234-236):
+// u += s*du; v = (v + s*dv) + (logc - trial); lc = logc over ld entries.
+cudaError_t launch_accept(otn_ctx* x, double s, double* u, const double* du, double* v,
+                          const double* dv, const double* logc, const double* trial, double* lc,
+                          const int* gate);
+// OTN_RED_ROW_STATS that also writes g = exp(a) - b (OTN_VEC_GRAD) to `g`.
+constexpr int kRedRowStatsGrad = 100;
 cudaError_t launch_step_gate(otn_ctx* x, int stage, const DevResult* res, const double* mass,
                              double slope_floor, double armijo_c1, int* flags);
 cudaError_t launch_round(otn_ctx* x, double* P, const double* C, const double* r, const double* c,

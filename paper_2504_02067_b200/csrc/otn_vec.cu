@@ -60,8 +60,10 @@ __global__ void __launch_bounds__(1024) k_reduce(int op, int64_t n, const double
   int f = 0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     switch (op) {
+      case kRedRowStatsGrad:
       case OTN_RED_ROW_STATS: {
         const double x = exp_fast(a[i]), y = b[i];
+        if (op == kRedRowStatsGrad) const_cast<double*>(c)[i] = __dsub_rn(x, y);   // VEC_GRAD
         s0 += fabs(__dsub_rn(x, y));
         s1 += __ddiv_rn(__dmul_rn(y, y), x);
         if (x <= 0.0) f |= 1;
@@ -252,6 +254,29 @@ cudaError_t launch_reduce(otn_ctx* x, int op, int64_t n, const double* a, const 
                           const double* c, const double* d, double* dst, int* flag,
                           const int* gate) {
   k_reduce<<<1, 1024, 0, x->stream>>>(op, n, a, b, c, d, dst, flag, gate);
+  return cudaGetLastError();
+}
+
+__global__ void k_accept(int64_t n, int64_t ld, double s, double* u, const double* du, double* v,
+                         const double* dv, const double* logc, const double* trial, double* lc,
+                         const int* gate) {
+  if (gate && *gate == 0) return;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < ld;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    if (i < n) {
+      u[i] = __dadd_rn(u[i], __dmul_rn(s, du[i]));                                   // VEC_AXPY
+      v[i] = __dadd_rn(__dadd_rn(v[i], __dmul_rn(s, dv[i])), __dsub_rn(logc[i], trial[i]));
+    }
+    lc[i] = logc[i];                                                                 // VEC_COPY
+  }
+}
+
+cudaError_t launch_accept(otn_ctx* x, double s, double* u, const double* du, double* v,
+                          const double* dv, const double* logc, const double* trial, double* lc,
+                          const int* gate) {
+  const int64_t blocks = std::min<int64_t>((x->ld + 255) / 256, 4 * x->num_sms);
+  k_accept<<<unsigned(std::max<int64_t>(blocks, 1)), 256, 0, x->stream>>>(x->n, x->ld, s, u, du, v,
+                                                                         dv, logc, trial, lc, gate);
   return cudaGetLastError();
 }
 
