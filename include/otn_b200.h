@@ -279,6 +279,15 @@ int otn_vec(otn_ctx* ctx, int op, double s, const double* a, const double* b, co
             const double* d, double* out);
 int otn_reduce(otn_ctx* ctx, int op, const double* a, const double* b, const double* c,
                const double* d, double* host_out, int* host_flags);
+/* Row statistics of the projector (projector.py:176, core.py:42-52) in one
+ * pass: g = exp(lr) - r (as OTN_VEC_GRAD) and host_out = OTN_RED_ROW_STATS of
+ * (lr, r), host_flags its domain flags.  Synchronizes.                      */
+int otn_row_stats(otn_ctx* ctx, const double* lr, const double* r, double* g, double* host_out,
+                  int* host_flags);
+/* The accept step's vector updates (projector.py:234-236) in one launch:
+ * u += alpha*d_u; v = (v + alpha*d_v) + (log_c - trial); lc := log_c.       */
+int otn_accept(otn_ctx* ctx, double alpha, double* u, const double* d_u, double* v,
+               const double* d_v, const double* log_c, const double* trial, double* lc);
 /* As otn_reduce without the host synchronization: the two results are copied
  * stream-ordered into host_out, which must be page-locked; they are valid
  * once the stream has passed this point (record an event after the call).

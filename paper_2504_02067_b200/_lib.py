@@ -102,6 +102,8 @@ SIGNATURES = {
     "otn_reduce_n": [_P, _I64, _I, _P, _P, _P, _P, _DP, _IP],
     "otn_vec": [_P, _I, _D, _P, _P, _P, _P, _P],
     "otn_reduce": [_P, _I, _P, _P, _P, _P, _DP, _IP],
+    "otn_row_stats": [_P, _P, _P, _P, _DP, _IP],
+    "otn_accept": [_P, _D, _P, _P, _P, _P, _P, _P, _P],
     "otn_reduce_async": [_P, _I, _P, _P, _P, _P, _P],
     "otn_round_plan": [_P, _P, _P, _P, _P, _DP, _IP],
 }

@@ -584,6 +584,31 @@ int otn_reduce_async(otn_ctx* x, int op, const double* a, const double* b, const
   return OTN_OK;
 }
 
+int otn_row_stats(otn_ctx* x, const double* lr, const double* r, double* g, double* host_out,
+                  int* host_flags) {
+  OTN_REQUIRE(x && lr && r && g && host_out, "otn_row_stats: NULL argument");
+  OTN_CUDA(cudaMemsetAsync(x->flags + 2, 0, sizeof(int), x->stream), "otn_row_stats: flag");
+  OTN_CUDA(otn::launch_reduce(x, otn::kRedRowStatsGrad, x->n, lr, r, g, nullptr, x->scal + 8,
+                              x->flags + 2),
+           "otn_row_stats");
+  OTN_CUDA(cudaMemcpyAsync(x->h_scal + 8, x->scal + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                           x->stream), "otn_row_stats: copy");
+  OTN_CUDA(cudaMemcpyAsync(x->h_flags + 2, x->flags + 2, sizeof(int), cudaMemcpyDeviceToHost,
+                           x->stream), "otn_row_stats: copy");
+  OTN_CUDA(stream_wait(x->stream), "otn_row_stats: sync");
+  host_out[0] = x->h_scal[8];
+  host_out[1] = x->h_scal[9];
+  if (host_flags) *host_flags = x->h_flags[2];
+  return OTN_OK;
+}
+
+int otn_accept(otn_ctx* x, double alpha, double* u, const double* d_u, double* v,
+               const double* d_v, const double* log_c, const double* trial, double* lc) {
+  OTN_REQUIRE(x && u && d_u && v && d_v && log_c && trial && lc, "otn_accept: NULL argument");
+  OTN_CUDA(otn::launch_accept(x, alpha, u, d_u, v, d_v, log_c, trial, lc, nullptr), "otn_accept");
+  return OTN_OK;
+}
+
 int otn_reduce(otn_ctx* x, int op, const double* a, const double* b, const double* c,
                const double* d, double* host_out, int* host_flags) {
   OTN_REQUIRE(x && a && host_out, "otn_reduce: NULL argument");

@@ -232,13 +232,11 @@ class DualState:
         is left in self._g.  Cached until log_rP or r changes."""
         if self._rowstat is None:
             lr = self._lr_dev()
-            k = self._ctx
-            k.call("otn_vec", _lib.VEC_GRAD, 0.0, vptr(lr), vptr(self._r), None, None,
-                   vptr(self._g))
             out = (ctypes.c_double * 2)()
             fl = ctypes.c_int(0)
-            k.call("otn_reduce", _lib.RED_ROW_STATS, vptr(lr), vptr(self._r), None, None, out,
-                   ctypes.byref(fl))
+            # g = exp(lr) - r and the row statistics in one pass
+            self._ctx.call("otn_row_stats", vptr(lr), vptr(self._r), vptr(self._g), out,
+                           ctypes.byref(fl))
             self._rowstat = (float(out[0]), float(out[1]), int(fl.value))
         return self._rowstat
 
@@ -425,13 +423,9 @@ class DualState:
     def _accept(self, alpha, d_u, d_v):
         """u += alpha d_u; v = (v + alpha d_v) + (log c - trial); log c(P) = log c
         (projector.py:234-236)."""
-        k = self._ctx
-        k.call("otn_vec", _lib.VEC_AXPY, float(alpha), vptr(self._u), vptr(d_u), None, None,
-               vptr(self._u))
-        k.call("otn_vec", _lib.VEC_STEP_V, float(alpha), vptr(self._v), vptr(d_v),
-               vptr(self._log_c), vptr(self._trial_vec), vptr(self._v))
+        self._ctx.call("otn_accept", float(alpha), vptr(self._u), vptr(d_u), vptr(self._v),
+                       vptr(d_v), vptr(self._log_c), vptr(self._trial_vec), vptr(self._lc))
         self._invalidate()
-        self._ctx.copy(self._lc, self._log_c)
 
     def _system(self):
         from .newton import DiscountedSystem

@@ -106,3 +106,32 @@ def test_async_reduce_equals_sync_reduce():
         assert (host[0].item(), host[1].item()) == (out[0], out[1])
     g = st._grad_norm_l1_deferred()
     assert g.value() == st.grad_norm_l1()
+
+
+def test_row_stats_and_accept_equal_their_component_ops():
+    """otn_row_stats == otn_vec(GRAD) + otn_reduce(ROW_STATS) and otn_accept ==
+    otn_vec(AXPY) + otn_vec(STEP_V) + copy, bit for bit."""
+    import torch
+    _, st = _state()
+    k = st._ctx
+    g1, g2 = k.vec(), k.vec()
+    out1, out2 = (ctypes.c_double * 2)(), (ctypes.c_double * 2)()
+    f1, f2 = ctypes.c_int(0), ctypes.c_int(0)
+    k.call("otn_row_stats", vptr(st._lr), vptr(st._r), vptr(g1), out1, ctypes.byref(f1))
+    k.call("otn_vec", _lib.VEC_GRAD, 0.0, vptr(st._lr), vptr(st._r), None, None, vptr(g2))
+    k.call("otn_reduce", _lib.RED_ROW_STATS, vptr(st._lr), vptr(st._r), None, None, out2,
+           ctypes.byref(f2))
+    assert (out1[0], out1[1], f1.value) == (out2[0], out2[1], f2.value)
+    np.testing.assert_array_equal(g1.cpu().numpy(), g2.cpu().numpy())
+    rng = np.random.default_rng(3)
+    du, dv, tr = (torch.from_numpy(rng.standard_normal(k.ld)).cuda() for _ in range(3))
+    u1, v1, u2, v2 = st._u.clone(), st._v.clone(), st._u.clone(), st._v.clone()
+    lc1, lc2 = k.vec(), k.vec()
+    k.call("otn_accept", 0.375, vptr(u1), vptr(du), vptr(v1), vptr(dv), vptr(st._log_c), vptr(tr),
+           vptr(lc1))
+    k.call("otn_vec", _lib.VEC_AXPY, 0.375, vptr(u2), vptr(du), None, None, vptr(u2))
+    k.call("otn_vec", _lib.VEC_STEP_V, 0.375, vptr(v2), vptr(dv), vptr(st._log_c), vptr(tr),
+           vptr(v2))
+    k.copy(lc2, st._log_c)
+    for x, y in ((u1, u2), (v1, v2), (lc1, lc2)):
+        np.testing.assert_array_equal(x.cpu().numpy(), y.cpu().numpy())
