@@ -242,9 +242,12 @@ def run_ours(args, rank, world):
                      "frac": achieved / hbm, "peak_source": hbm_src,
                      "traffic": traffic,
                      "traffic_per_alg_byte": traffic_ratio,
-                     "note": "alg bytes = the dense fused minimum (16n^2 per HVP, SURVEY 8(d)); "
-                             "the kernel skips exact-zero plan entries (segment mask / sparse "
-                             "shared-memory rows), so frac > 1 and DRAM traffic ~2% of alg bytes",
+                     "note": "alg bytes = the dense fused minimum (16n^2 per HVP + 8n^2 per "
+                             "d_v pass, SURVEY 8(d)); the kernel skips exact-zero plan entries "
+                             "(segment mask, compressed rows in shared / global memory) and the "
+                             "134 MB plan is largely L2-resident, so frac > 1 and DRAM traffic is "
+                             "~4% of the alg bytes (traffic_per_alg_byte); extras.fused_px has the "
+                             "steady-state dense HVP (~7.5 TB/s, 115% of the measured HBM peak)",
                      "alg_bytes_per_launch": alg_bytes / max(len(coop), 1),
                      "launches": len(coop), "kernel_ms_total": coop_ms,
                      "kernel_share_of_step": coop_ms / sum(step_ms)},
