@@ -58,7 +58,7 @@ LAUNCHES = {
     "otn_newton": 2, "otn_probe": 2,
     # newton (2) + gate + trial (1 | 2) + mass + gate + accept (u, v, lc) + row LSE
     # + row stats with the gradient
-    "otn_newton_step": 10,
+    "otn_newton_step": 9,
     "otn_vec": 1, "otn_reduce": 1, "otn_row_stats": 1, "otn_accept": 1, "otn_reduce_async": 1, "otn_round_plan": 10, "otn_pc_pass": 1,
     "otn_vec_n": 1, "otn_reduce_n": 1,
 }

@@ -464,13 +464,12 @@ int otn_newton_step(otn_ctx* x, const double* P, const uint64_t* m, const double
   a.d = d_u;
   a.dv = d_v;
   a.pre_flags = x->flags;
+  a.step_flags = x->flags + 6;                      // the first gate is set by k_coop itself
   OTN_CUDA(otn::launch_coop(x, a), "otn_newton_step");
   // scalars: scal[32] trial mass, scal[33..34] row statistics;
   // flags[6] trial gate, flags[7] accept gate, flags[8] row-statistics flags
   int* gates = x->flags + 6;
   const int n = int(x->n);
-  OTN_CUDA(otn::launch_step_gate(x, 0, x->dres, nullptr, slope_floor, armijo_c1, gates),
-           "otn_newton_step: gate");
   cudaError_t e = sym ? otn::launch_lse_rows(x, Ccols, ng, v, d_v, u, d_u, 1.0, 0, trial, gates)
                       : otn::launch_lse_cols(x, Ccols, ng, v, d_v, u, d_u, 1.0, 0, trial, gates);
   OTN_CUDA(e, "otn_newton_step: trial");

@@ -1174,6 +1174,16 @@ __device__ void column_pass(cg::grid_group& grid, const CoopArgs& a, double xv, 
   phase_a2(a, kind, out, sh);
 }
 
+// The launch result; for otn_newton_step also its first gate (the direction
+// is usable: status OK and slope > 0), which k_step_gate stage 0 would compute.
+__device__ __forceinline__ void publish_result(const CoopArgs& a, const DevResult& res) {
+  *a.res = res;
+  if (a.step_flags) {
+    a.step_flags[0] = res.status == OTN_OK && res.slope > 0.0;
+    a.step_flags[2] = 0;
+  }
+}
+
 __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
   __shared__ Smem sh;
   cg::grid_group grid = cg::this_grid();
@@ -1199,7 +1209,7 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
     if (f0) res.status = OTN_ST_PLAN_OVERFLOW;
     else if (f1) res.status = OTN_ST_NONPOSITIVE_SUMS;
     if (res.status != OTN_OK) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) *a.res = res;
+      if (blockIdx.x == 0 && threadIdx.x == 0) publish_result(a, res);
       return;  // uniform across the grid: no barrier is skipped by only some CTAs
     }
   }
@@ -1304,7 +1314,7 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
     if (row.own) a.d[row.i] = sh.sv[threadIdx.x];
   }
   res.hvps = nh;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *a.res = res;
+  if (blockIdx.x == 0 && threadIdx.x == 0) publish_result(a, res);
 }
 
 static_assert(kRingBytes == size_t(kRingDepth) * kSlotBytes, "ring layout");

@@ -104,6 +104,7 @@ struct CoopArgs {
   // workspace
   double *r, *z, *p, *q, *M, *wc, *sv, *wpart, *red;
   DevResult* res;
+  int* step_flags;        // nullable: otn_newton_step's gate words (see k_step_gate stage 0)
 };
 cudaError_t launch_coop(otn_ctx* x, const CoopArgs& a);
 size_t sparse_g_bytes_per_cta();        // kPlanSparseG buffer slice (allocated when ld <= 4096)
