@@ -135,3 +135,24 @@ def test_row_stats_and_accept_equal_their_component_ops():
     k.copy(lc2, st._log_c)
     for x, y in ((u1, u2), (v1, v2), (lc1, lc2)):
         np.testing.assert_array_equal(x.cpu().numpy(), y.cpu().numpy())
+
+
+def test_newton_step_column_kernels_path():
+    """otn_newton_step with symmetric = 0 (the trial through the two-kernel
+    column LSE on C itself, gated) equals the per-call path on the same
+    asymmetric cost."""
+    _, a = _state("pix:256:784:0", 2.0 ** 9)
+    _, b = _state("pix:256:784:0", 2.0 ** 9)
+    for st in (a, b):
+        st._row_grad_norm()
+        C = st._dc.C
+        st._dc.col_args = (lambda C=C: (vptr(C), 0))     # no transpose: column kernels
+    da, dva = a._dir_bufs()
+    db, dvb = b._dir_bufs()
+    res_a, mass_a, _ = _newton_step_device(a, a._system(), a._g, 0.5, 0.0, False, None, da, dva,
+                                           ARMIJO_C1, ARMIJO_SLOPE_FLOOR)
+    res_b = _newton_device(b._g, b._system(), 0.5, 0.0, False, None, db, dvb)
+    assert res_a.status == res_b.status == _lib.OTN_OK
+    mass_b = b._trial(db, dvb, 1.0, b._trial_buf())
+    assert mass_a == mass_b
+    np.testing.assert_array_equal(a._trial_vec.cpu().numpy(), b._trial_vec.cpu().numpy())
