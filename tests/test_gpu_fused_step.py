@@ -156,3 +156,26 @@ def test_newton_step_column_kernels_path():
     mass_b = b._trial(db, dvb, 1.0, b._trial_buf())
     assert mass_a == mass_b
     np.testing.assert_array_equal(a._trial_vec.cpu().numpy(), b._trial_vec.cpu().numpy())
+
+
+def test_persistent_launch_timing():
+    """otn_set_timing / otn_coop_ms: device time of the last persistent launch
+    (the bench's roofline source); an error while timing is off."""
+    from paper_2504_02067_b200._device import TELEMETRY
+    from paper_2504_02067_b200.errors import OTNError
+    _, st = _state()
+    st._row_grad_norm()
+    d, dv = st._dir_bufs()
+    TELEMETRY.reset()
+    TELEMETRY.time_coop = True
+    try:
+        res, _, _ = _newton_step_device(st, st._system(), st._g, 0.5, 0.0, False, None, d, dv,
+                                        ARMIJO_C1, ARMIJO_SLOPE_FLOOR)
+        ms, hvps, dvflag, n = TELEMETRY.coop[-1]
+        assert ms > 0.0 and hvps == res.hvps and n == st.n
+    finally:
+        TELEMETRY.time_coop = False
+    k = st._ctx
+    assert k.coop_timing() is False
+    with pytest.raises(OTNError):
+        k.coop_ms()
