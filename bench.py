@@ -2,33 +2,43 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload (configs[1] of BASELINE.json, the metric's configuration): D2, n = 4096
-(64x64 pixel grid), squared-L2 cost, smooth-random marginals (seeds 0 / 1),
-MDOT annealing gamma 2^5 -> 2^16 until ||r(P)-r||_1 + ||c(P)-c||_1 <= 1e-6.
-One step = one complete ``mdot`` solve (all stages, final plan, rounding,
-primal cost).  The metric is seconds per solve (lower is better).
+N = 1 (the metric's configuration, BASELINE configs[1]): D2 -- n = 4096 (64x64
+pixel grid), squared-L2 cost, smooth-random marginals (seeds 0 / 1), MDOT
+annealing gamma 2^5 -> 2^16 until ||r(P)-r||_1 + ||c(P)-c||_1 <= 1e-6.  One
+step = one complete ``mdot`` solve (all stages, final plan, rounding, primal
+cost); the metric is seconds per solve (lower is better).
 
-  value  device-resident: C already in HBM (a CUDA tensor problem); CUDA
-         events bracket each solve on the solver stream; L2 is flushed
-         (512 MB write) between steps, and the 134 MB cost is itself > L2.
-  e2e    the same solve through the public API with a HOST numpy problem:
-         the 134 MB cost H2D, the solve, and the 134 MB rounded plan D2H all
-         inside the timed region (bytes counted by the package).
-  roofline  the persistent CG/Newton kernel (k_coop), the dominant kernel:
-         algorithmic bytes = 16 n^2 per Hessian-vector product (two streaming
-         passes over the plan) + 8 n^2 for the d_v back-substitution, summed
-         over the launches of the timed region / their summed CUDA-event time.
-  cpu_baseline  the bit-exact oracle port of the reference (oracle/), all host
-         threads for BLAS: a bounded sample of each dense primitive on the
-         same n = 4096 problem, scaled by the reference's own primitive-call
-         counts for this solve (tests/golden/callmix_*.json).
+  value     device-resident: C already in HBM (a CUDA tensor problem); CUDA
+            events bracket each solve on the solver stream; L2 is flushed
+            (512 MB write) between steps, and the 134 MB cost is itself > L2.
+  e2e       the same solve through the public API with a HOST (page-locked)
+            problem: the 134 MB cost H2D, the solve, and the 134 MB rounded
+            plan D2H all inside the timed region (bytes counted by the package).
+  parity    the timed configuration against the reference's own trajectory
+            (tests/golden/traj_D2_grid64_l2sq_s0.npz, produced by the reference):
+            stages, CG iterations, u / v inf-norm-relative differences.
+  roofline  the persistent CG/Newton kernel (k_coop), the dominant kernel,
+            against the bytes each launch has to stream: per HVP two passes
+            over the plan entries inside the rows' nonzero 64-column segments
+            (ring mode, HBM / L2) or over the compressed nonzeros (value +
+            column index, modes 2 / 3: shared memory / L2) -- what the kernel
+            actually reads, not the dense 16 n^2; peak = measured HBM copy
+            bandwidth.  ``traffic`` = ncu DRAM bytes per launch.
+  cpu_baseline  complete solves of the reference's CPU path (the bit-exact
+            oracle port of otnewton.mdot, oracle/) on the host cores: OpenBLAS
+            and the oracle's 256-row slabs on all threads.
 
-Multi-GPU (--gpus N under torchrun): the headline n = 4096 solve runs as
-replicas (it does not shard profitably): each rank solves its own
-seed, value is the max-over-ranks time per solve divided by N.  The sharded
-path is measured in ``extras.d4``: D4 (n = 65536 3-D points, on-the-fly cost)
-row-sharded over all N ranks, with one NCCL allreduce per column-direction
-product (max-over-ranks wall time).  ``extras`` also times D1 and D3 at N = 1.
+N > 1 (``--gpus N`` re-executes itself under torch.distributed.run when not
+already launched that way): the headline is the ROW-SHARDED on-the-fly solve
+D4 (BASELINE configs[3]): n = 65536 3-D points, L2^2 cost recomputed in every
+pass, gamma 2^5 -> 2^10, rank g owning rows [g n/N, (g+1) n/N) with one NCCL
+allreduce per column-direction product; strong scaling (same n at every N);
+value = max over ranks of the solve time.  ``extras.d4_1gpu`` is the same solve
+on rank 0's GPU alone (the scaling reference), ``extras.d2_replicas`` the D2
+solve on every rank independently.
+
+--impl reference: the reference's CPU path (the oracle port) timed on full
+solves of the same workload on the host cores (rank 0 only).
 """
 
 from __future__ import annotations
@@ -37,6 +47,7 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import time
 
@@ -45,26 +56,41 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = dict(spec="grid:64:l2sq:{seed}", gamma_i=2.0 ** 5, gamma_f=2.0 ** 16, p=1.5, q_init=2.0)
-CALLMIX = os.path.join(ROOT, "tests", "golden", "callmix_D2_grid64_l2sq_s0.json")
 METRIC = "sec to ||r(P)-r||_1+||c(P)-c||_1<=1e-6 (n=4096)"
+METRIC_D4 = "sec to solve n=65536 on-the-fly 3-D OT (gamma 2^5->2^10), row-sharded"
+D2 = dict(spec="grid:64:l2sq:0", gamma_i=2.0 ** 5, gamma_f=2.0 ** 16, p=1.5, q_init=2.0)
+D2_GOLDEN = os.path.join(ROOT, "tests", "golden", "traj_D2_grid64_l2sq_s0.npz")
+D4_GAMMA = (2.0 ** 5, 2.0 ** 10)
 L2_FLUSH_BYTES = 512 << 20
 
+CONFIG_D2 = {
+    "workload": "D2 n=4096 grid64 L2^2 smooth-random seeds 0/1 gamma 2^5->2^16 to 1e-6",
+    "n": 4096, "gamma_i": D2["gamma_i"], "gamma_f": D2["gamma_f"], "p": 1.5, "q_init": 2.0,
+    "parallelism": "single",
+    "l2": "flushed between steps (512 MB write); C and P are 134 MB > L2",
+}
 
-def peaks():
+
+def config_d4(n, world):
+    return {"workload": f"D4 n={n} 3-D uniform points on-the-fly L2^2 gamma 2^5->2^10",
+            "n": n, "gamma_i": D4_GAMMA[0], "gamma_f": D4_GAMMA[1],
+            "parallelism": f"rows{world}",
+            "l2": "no n x n array exists: every pass recomputes the cost from the points"}
+
+
+def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            d = json.load(fh)
-        return float(d["hbm_gbs"]), "measured"
+            return json.load(fh), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return 6650.0, "fallback"
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
 # ---------------------------------------------------------------------------
-# clocks during the timed region (NVML)
+# clocks during the timed region
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi in a SUBPROCESS (no GIL contention with the solver's host
+    """nvidia-smi in a subprocess (no GIL contention with the solver's host
     loop) sampling SM clocks and throttle reasons every 200 ms."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
@@ -77,7 +103,6 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
-        import subprocess
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -117,22 +142,92 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# our arm
+# roofline of the persistent solver from its launch records
 # ---------------------------------------------------------------------------
-def run_ours(args, rank, world):
+# bytes per compressed nonzero per pass: the value (8) and its column / row
+# index (2, u16) -- the CSR for P w, the CSC for P^T x
+SPARSE_BYTES_PER_NNZ = 10
+MODE_NAMES = {0: "ring (streamed spans)", 2: "compressed rows, shared memory",
+              3: "compressed rows, global memory (L2)"}
+
+
+def kcoop_roofline(coop, peak_gbs, n):
+    """Per-mode and total roofline of k_coop from TELEMETRY.coop records
+    (ms, hvps, dv, n, mode, nnz, span, cg)."""
+    per_mode = {}
+    tot_bytes = tot_ms = 0.0
+    for (ms, hvps, dv, _n, mode, nnz, span, cg) in coop:
+        if mode == 0:
+            # each HVP streams the spans twice (P^T x, then P w); d_v once more
+            b = 8.0 * span * (2 * hvps + dv)
+        else:
+            # compression reads the spans once; then every pass walks the
+            # compressed nonzeros (value + index)
+            b = 8.0 * span + SPARSE_BYTES_PER_NNZ * nnz * (2 * hvps + dv)
+        m = per_mode.setdefault(mode, {"launches": 0, "hvps": 0, "cg_iters": 0, "ms": 0.0,
+                                       "bytes": 0.0, "nnz_mean": 0.0})
+        m["launches"] += 1
+        m["hvps"] += hvps
+        m["cg_iters"] += cg
+        m["ms"] += ms
+        m["bytes"] += b
+        m["nnz_mean"] += nnz
+        tot_bytes += b
+        tot_ms += ms
+    for mode, m in per_mode.items():
+        m["nnz_mean"] /= max(m["launches"], 1)
+        m["gbps"] = m["bytes"] / (m["ms"] * 1e-3) / 1e9 if m["ms"] > 0 else 0.0
+        m["frac_of_hbm_peak"] = m["gbps"] / peak_gbs
+        m["us_per_hvp"] = m["ms"] * 1e3 / max(m["hvps"], 1)
+        m["path"] = MODE_NAMES.get(mode, str(mode))
+    achieved = tot_bytes / (tot_ms * 1e-3) / 1e9 if tot_ms > 0 else 0.0
+    return achieved, tot_bytes, tot_ms, {str(k): v for k, v in sorted(per_mode.items())}
+
+
+def kcoop_traffic():
+    """ncu DRAM bytes per k_coop launch of one D2 solve (profiles/, tools/kcoop_dram.py)."""
+    path = os.path.join(ROOT, "profiles", "kcoop_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        return json.load(fh).get("dram_bytes_per_launch")
+
+
+# ---------------------------------------------------------------------------
+# our arm, N = 1: D2
+# ---------------------------------------------------------------------------
+def parity_block(sol, prob):
+    """The timed configuration against the reference's own trajectory."""
+    z = np.load(D2_GOLDEN, allow_pickle=False)
+    meta = json.loads(str(z["meta"]))
+    st = sol.final_state
+    u, v = st.u, st.v
+    du = float(np.abs(u - z["u"]).max() / np.abs(z["u"]).max())
+    dv = float(np.abs(v - z["v"]).max() / np.abs(z["v"]).max())
+    st.set_targets(prob.r, prob.c)
+    ss = meta["self_spread"]
+    return {"stages": len(sol.iterations), "stages_ref": len(meta["stages"]),
+            "cg_iters": sum(i.stats.cg_iters for i in sol.iterations),
+            "cg_iters_ref": meta["totals"]["cg"],
+            "cg_iters_ref_deterministic": ss["cg_total"],
+            "newton_steps": sum(i.stats.newton_steps for i in sol.iterations),
+            "newton_steps_ref": meta["totals"]["newton"],
+            "du_rel": du, "dv_rel": dv, "ref_self_spread_du": ss["du"],
+            "ref_self_spread_dv": ss["dv"],
+            "primal_rel": abs(sol.primal_cost - meta["primal"]) / abs(meta["primal"]),
+            "true_marginal_err": st.grad_norm_l1(), "target": 1e-6}
+
+
+def run_d2(args, dev):
     import torch
 
     import paper_2504_02067_b200 as ot
     from paper_2504_02067_b200._device import TELEMETRY
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
-    torch.cuda.set_device(dev)
-    seed = rank  # replicas: one seed per rank
-    host_prob = ot.workload(WORKLOAD["spec"].format(seed=seed))
+    host_prob = ot.workload(D2["spec"])
     n = host_prob.n
-    # e2e inputs come from page-locked host memory (the contract's H2D source)
     pinned_C = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-    pinned_C.numpy()[:] = host_prob.C
+    pinned_C.numpy()[:] = host_prob.C                    # e2e H2D source: page-locked
     host_prob = ot.Problem(C=pinned_C.numpy(), r=host_prob.r, c=host_prob.c, label=host_prob.label)
     dprob = ot.Problem(C=torch.from_numpy(host_prob.C).to(dev), r=host_prob.r, c=host_prob.c,
                        label=host_prob.label)
@@ -140,40 +235,35 @@ def run_ours(args, rank, world):
     stream = torch.cuda.current_stream(dev)
 
     def solve(prob):
-        return ot.mdot(prob, WORKLOAD["gamma_i"], WORKLOAD["gamma_f"], p=WORKLOAD["p"],
-                       q_init=WORKLOAD["q_init"])
+        return ot.mdot(prob, D2["gamma_i"], D2["gamma_f"], p=D2["p"], q_init=D2["q_init"])
 
     for _ in range(args.warmup):
         solve(dprob)
     torch.cuda.synchronize()
-    barrier(world)
 
-    # ---- device-resident timed region ------------------------------------
+    # ---- device-resident timed region --------------------------------------
     TELEMETRY.reset()
     TELEMETRY.time_coop = True
     step_ms = []
-    sols = []
     with ClockSampler(dev.index) as clocks:
         torch.cuda.synchronize()
         for _ in range(args.steps):
-            flush.fill_(1.0)                         # evict L2 between steps (untimed)
+            flush.fill_(1.0)                             # evict L2 between steps (untimed)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             sol = solve(dprob)
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
-            del sol                                  # a held result would pin a 134 MB plan
-                                                     # buffer and force fresh allocations
+            del sol                                      # a held result pins a 134 MB plan
         torch.cuda.synchronize()
     TELEMETRY.time_coop = False
     launches = TELEMETRY.launches
     coop = list(TELEMETRY.coop)
     calls = dict(TELEMETRY.calls)
-    barrier(world)
 
     # ---- e2e through the public API with host buffers ------------------------
-    _warm = solve(host_prob)              # warm the page-locked result buffer (untimed)
+    _warm = solve(host_prob)                             # warm the page-locked result buffer
     del _warm
     TELEMETRY.reset()
     e2e_ms = []
@@ -181,7 +271,7 @@ def run_ours(args, rank, world):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        sol_h = solve(host_prob)          # H2D of C inside, D2H of the rounded P inside
+        sol_h = solve(host_prob)                         # H2D of C inside, D2H of P inside
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
         if len(e2e_ms) < args.steps:
@@ -189,35 +279,22 @@ def run_ours(args, rank, world):
     h2d = TELEMETRY.h2d / args.steps
     d2h = TELEMETRY.d2h / args.steps
 
-    # ---- precision check of the timed solves (after the timed region) -----
-    sols.append(solve(dprob))             # one more (untimed) solve for the precision check
-    errs = []
-    for s in sols[:1] + [sol_h]:
-        st = s.final_state
-        st.set_targets(host_prob.r, host_prob.c)
-        errs.append(st.grad_norm_l1())
+    # ---- parity of the timed configuration (after the timed regions) -------
+    sol = solve(dprob)
+    parity = parity_block(sol, host_prob)
+    st = sol_h.final_state
+    st.set_targets(host_prob.r, host_prob.c)
+    parity["true_marginal_err_e2e"] = st.grad_norm_l1()
 
-    # ---- roofline of the dominant kernel -------------------------------------
-    nn8 = float(n) * n * 8.0            # one pass over the n x n float64 plan
-    alg_bytes = sum(2.0 * nn8 * h + nn8 * dv for (_, h, dv, _) in coop)
-    coop_ms = sum(ms for (ms, _, _, _) in coop)
-    hbm, hbm_src = peaks()
-    achieved = alg_bytes / (coop_ms * 1e-3) / 1e9 if coop_ms > 0 else 0.0
-    traffic = traffic_ratio = None
-    tpath = os.path.join(ROOT, "profiles", "kcoop_traffic.json")
-    if os.path.exists(tpath):                # ncu capture of the same solve (tools/kcoop_dram.py)
-        with open(tpath) as fh:
-            tj = json.load(fh)
-        traffic = tj.get("dram_bytes_per_launch")
-        traffic_ratio = tj.get("traffic_bytes_per_alg_byte")
-
-    ms = max_over_ranks(statistics.mean(step_ms), world)
-    e2e = max_over_ranks(statistics.mean(e2e_ms), world)
+    peaks, peak_src = load_peaks()
+    hbm = float(peaks["hbm_gbs"])
+    achieved, alg_bytes, coop_ms, modes = kcoop_roofline(coop, hbm, n)
+    ms = statistics.mean(step_ms)
     out = {
         "metric": METRIC,
-        "value": ms / 1e3 / world,
+        "value": ms / 1e3,
         "unit": "s",
-        "n_gpus": world,
+        "n_gpus": 1,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms,
@@ -226,62 +303,51 @@ def run_ours(args, rank, world):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded 64x64 grid cost + smooth-random marginals, reference generators)",
-        "config": {"workload": "D2 n=4096 grid64 L2^2 seed=rank gamma 2^5->2^16 to 1e-6",
-                   "n": n, "gamma_i": WORKLOAD["gamma_i"], "gamma_f": WORKLOAD["gamma_f"],
-                   "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "flushed between steps (512 MB write); C and P are 134 MB > L2",
-                   "stages": len(sols[0].iterations),
-                   "cg_iters": sum(i.stats.cg_iters for i in sols[0].iterations),
-                   "true_marginal_err": errs[0]},
-        "e2e": {"value": e2e / 1e3 / world, "unit": "s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h)},
+        "config": dict(CONFIG_D2),
+        "e2e": {"value": statistics.mean(e2e_ms) / 1e3, "unit": "s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / max(args.steps, 1),
-        "roofline": {"bound": "hbm", "kernel": "k_coop (persistent CG/Newton)",
-                     "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "peak_source": hbm_src,
-                     "traffic": traffic,
-                     "traffic_per_alg_byte": traffic_ratio,
-                     "note": "alg bytes = the dense fused minimum (16n^2 per HVP + 8n^2 per "
-                             "d_v pass, SURVEY 8(d)); the kernel skips exact-zero plan entries "
-                             "(segment mask, compressed rows in shared / global memory) and the "
-                             "134 MB plan is largely L2-resident, so frac > 1 and DRAM traffic is "
-                             "~4% of the alg bytes (traffic_per_alg_byte); extras.fused_px has the "
-                             "steady-state dense HVP (~7.5 TB/s, 115% of the measured HBM peak)",
-                     "alg_bytes_per_launch": alg_bytes / max(len(coop), 1),
-                     "launches": len(coop), "kernel_ms_total": coop_ms,
-                     "kernel_share_of_step": coop_ms / sum(step_ms)},
+        "parity": parity,
+        "roofline": {
+            "bound": "hbm", "kernel": "k_coop (persistent CG/Newton)",
+            "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "peak_source": peak_src,
+            "traffic": kcoop_traffic(),
+            "basis": "bytes each launch must stream: ring mode 8 B x span entries per pass "
+                     "(2 passes per HVP + 1 for d_v); compressed modes 8 B x span once + "
+                     f"{SPARSE_BYTES_PER_NNZ} B x nnz per pass (value + u16 index, from shared "
+                     "memory / L2); traffic = ncu dram__bytes per launch (profiles/)",
+            "alg_bytes_per_launch": alg_bytes / max(len(coop), 1),
+            "launches": len(coop), "kernel_ms_total": coop_ms,
+            "kernel_share_of_step": coop_ms / sum(step_ms),
+            "per_mode": modes,
+        },
         "clocks": clocks.summary(),
         "per_step_ms": step_ms,
         "e2e_per_step_ms": e2e_ms,
         "calls_per_step": {k: v / args.steps for k, v in calls.items()},
     }
-    if not args.no_extras:
-        out["extras"] = run_extras(args, rank, world, dev)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:   # N = 1 only (contract)
-        out["cpu_baseline"] = cpu_baseline(host_prob, budget_s=args.cpu_budget)
     return out
 
 
-# FP64-pipe instructions per plan entry in the on-the-fly pair kernel at d = 3
-# (ncu smsp__inst_executed_pipe_fp64 x 32 / entries at n = 65536: 31.1 for
-# the product pass, 33.2 for the log-sum-exp pass).
-PAIR_FP64_INSTR_PER_ENTRY = 32
+# ---------------------------------------------------------------------------
+# extras (N = 1): the other configurations, one timed solve each
+# ---------------------------------------------------------------------------
+PAIR_FP64_INSTR_PER_ENTRY = 32     # ncu: 31.1 (product pass) / 33.2 (log-sum-exp pass) at d = 3
 
 
-def fused_px(dev, reps=200):
-    """BASELINE's "fused P.x GB/s": steady-state time of one HVP (P^T x, A2,
-    P w: 16 n^2 algorithmic bytes) inside the persistent kernel, repeated
-    `reps` times in one launch on the D2 L2^2 plan of the first stage (dense,
-    gamma 2^5) and of the last (gamma 2^16, ~450 K nonzeros).  P (134 MB) is
-    about the L2 size, so part of the stream is served from L2."""
+def fused_px(dev, peak, reps=200):
+    """BASELINE's "fused P.x GB/s": steady-state time of one HVP (P^T x, the
+    column combine, P w) repeated inside one persistent launch on the D2 plan
+    of the first stage (dense) and of the last (~450 K nonzeros).  The dense
+    figure is effective bandwidth over 16 n^2 bytes; P (134 MB) is about the
+    L2 size, so part of the stream is served from L2."""
     import torch
 
     import paper_2504_02067_b200 as ot
     from paper_2504_02067_b200._device import vptr
-    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
-        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
-    p = ot.workload("grid:64:l2sq:0")
+    p = ot.workload(D2["spec"])
     dp = ot.Problem(C=torch.from_numpy(p.C).to(dev), r=p.r, c=p.c)
     res = {}
     for key, gf in (("dense_gamma_2^5", 2.0 ** 5), ("sparse_gamma_2^16", 2.0 ** 16)):
@@ -291,9 +357,9 @@ def fused_px(dev, reps=200):
         x = torch.randn(k.ld, dtype=torch.float64, device=dev)
         out = k.vec()
 
-        def go(n):
+        def go(reps_):
             k.call("otn_probe", vptr(s._P), vptr(s._mask), vptr(s._cP), vptr(s._rP), vptr(x),
-                   vptr(out), 5, n)
+                   vptr(out), 5, reps_)
         go(reps)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -302,151 +368,226 @@ def fused_px(dev, reps=200):
         e1.record()
         e1.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / reps
-        alg = 16.0 * p.n * p.n
-        res[key] = {"hvp_us": us, "alg_bytes": alg, "gbps": alg / (us * 1e-6) / 1e9,
-                    "frac_of_hbm_peak": alg / (us * 1e-6) / 1e9 / peak}
+        dense = 16.0 * p.n * p.n
+        res[key] = {"hvp_us": us, "effective_gbps_dense_bytes": dense / (us * 1e-6) / 1e9,
+                    "effective_frac_of_hbm_peak": dense / (us * 1e-6) / 1e9 / peak}
     res["peak_gbps"] = peak
     return res
 
 
-def run_extras(args, rank, world, dev):
-    """The other BASELINE configurations, one timed solve each (after a warm-up):
-    D1 (n=1024 2-D points, fixed gamma), D3 (n=4096 784-d pixel sets, stored C),
-    and D4 (n=65536 3-D points, on-the-fly cost) — row-sharded over all ranks
-    with NCCL allreduces when launched with --gpus N > 1."""
+def d4_solve(dev, n, comm=None):
+    """One timed D4 solve (cost object built outside the timed region);
+    returns (seconds, record)."""
     import torch
 
     import paper_2504_02067_b200 as ot
     from paper_2504_02067_b200._device import TELEMETRY
     from paper_2504_02067_b200.pointcloud import Comm, PointCloudCost
+    comm = comm or Comm()
+    pc = ot.points_problem(n, 3, 0)
+    cost = PointCloudCost(pc, dev, comm=comm)
+    TELEMETRY.reset()
+    torch.cuda.synchronize()
+    comm.barrier()
+    t0 = time.perf_counter()
+    sol = ot.mdot(pc, D4_GAMMA[0], D4_GAMMA[1], cost=cost)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    passes = TELEMETRY.calls.get("otn_pc_pass", 0)
+    st = sol.final_state
+    st.set_targets(pc.r, pc.c)
+    err = st.grad_norm_l1()
+    entries = float(n) * n * passes / comm.world        # per rank: n x n/world per pass
+    peak_entries = 148 * 64 * 1.965e9 / PAIR_FP64_INSTR_PER_ENTRY
+    rec = {"n": n, "dim": 3, "gamma": list(D4_GAMMA), "gpus": comm.world,
+           "sharding": f"rows over {comm.world} ranks" if comm.world > 1 else "none",
+           "stages": len(sol.iterations), "cg": sum(i.stats.cg_iters for i in sol.iterations),
+           "passes_per_rank": passes, "true_marginal_err": err, "primal": sol.primal_cost,
+           "collectives": dict(getattr(comm, "stats", {})),
+           "entries_per_s_per_gpu": entries / dt,
+           "fp64_pipe_frac_est": entries / dt / peak_entries,
+           "fp64_basis": f"{PAIR_FP64_INSTR_PER_ENTRY} FP64 instr/entry (SASS), "
+                         "64 FP64 instr/clk/SM x 148 SMs x 1.965 GHz"}
+    return dt, rec
+
+
+def run_extras(args, dev):
+    import torch
+
+    import paper_2504_02067_b200 as ot
     extras = {}
-
-    def timed(fn):
-        torch.cuda.synchronize()
-        barrier(world)
-        t0 = time.perf_counter()
-        res = fn()
-        torch.cuda.synchronize()
-        return res, max_over_ranks(time.perf_counter() - t0, world)
-
+    peaks, _ = load_peaks()
     try:
-        if world == 1:
-            for key, spec, gi, gf in (("d1_fixed", "pts:1024:2:0", 2.0 ** 10, 2.0 ** 10),
-                                      ("d3", "pix:4096:784:0", 2.0 ** 5, 2.0 ** 16)):
-                p = ot.workload(spec)
-                dp = ot.Problem(C=torch.from_numpy(p.C).to(dev), r=p.r, c=p.c)
-                ot.mdot(dp, gi, gf)
-                sol, dt = timed(lambda: ot.mdot(dp, gi, gf))
-                st = sol.final_state
-                st.set_targets(p.r, p.c)
-                extras[key] = {"spec": spec, "gamma": [gi, gf], "s": dt,
-                               "stages": len(sol.iterations),
-                               "cg": sum(i.stats.cg_iters for i in sol.iterations),
-                               "true_marginal_err": st.grad_norm_l1()}
-            extras["fused_px"] = fused_px(dev)
-        n4 = args.d4_n
-        pc = ot.points_problem(n4, 3, 0)
-        comm = Comm()
-
-        def d4():
-            cost = PointCloudCost(pc, dev, comm=comm)
-            return ot.mdot(pc, 2.0 ** 5, 2.0 ** 10, cost=cost)
-        if args.d4_warmup:
-            d4()
-        TELEMETRY.reset()
-        sol, dt = timed(d4)
-        passes = TELEMETRY.calls.get("otn_pc_pass", 0)
-        st = sol.final_state
-        st.set_targets(pc.r, pc.c)
-        err = st.grad_norm_l1()
-        entries = float(n4) * n4 * passes / world     # per rank (each pass covers n x n/world)
-        clk = 1.965e9
-        peak_entries = 148 * 64 * clk / PAIR_FP64_INSTR_PER_ENTRY
-        extras["d4"] = {"n": n4, "dim": 3, "gamma": [2.0 ** 5, 2.0 ** 10], "gpus": world,
-                        "sharding": "rows" if world > 1 else "none", "s": dt,
-                        "stages": len(sol.iterations),
-                        "cg": sum(i.stats.cg_iters for i in sol.iterations),
-                        "passes_per_rank": passes, "true_marginal_err": err,
-                        "primal": sol.primal_cost,
-                        "entries_per_s_per_gpu": entries / dt,
-                        "fp64_pipe_frac_est": entries / dt / peak_entries,
-                        "fp64_basis": f"{PAIR_FP64_INSTR_PER_ENTRY} FP64 instr/entry (SASS), "
-                                      "64 FP64 instr/clk/SM x 148 SMs x 1.965 GHz"}
-    except Exception as exc:                      # extras never break the headline line
+        for key, spec, gi, gf in (("d1_fixed", "pts:1024:2:0", 2.0 ** 10, 2.0 ** 10),
+                                  ("d3", "pix:4096:784:0", 2.0 ** 5, 2.0 ** 16)):
+            p = ot.workload(spec)
+            dp = ot.Problem(C=torch.from_numpy(p.C).to(dev), r=p.r, c=p.c)
+            ot.mdot(dp, gi, gf)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            sol = ot.mdot(dp, gi, gf)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            st = sol.final_state
+            st.set_targets(p.r, p.c)
+            extras[key] = {"spec": spec, "gamma": [gi, gf], "s": dt,
+                           "stages": len(sol.iterations),
+                           "cg": sum(i.stats.cg_iters for i in sol.iterations),
+                           "true_marginal_err": st.grad_norm_l1()}
+        extras["fused_px"] = fused_px(dev, float(peaks["hbm_gbs"]))
+        if args.d4_n:
+            dt, rec = d4_solve(dev, args.d4_n)
+            rec["s"] = dt
+            extras["d4_1gpu"] = rec
+    except Exception as exc:                              # extras never break the headline
         extras["error"] = f"{type(exc).__name__}: {exc}"
     return extras
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline / reference arm: the oracle port on the host cores
+# our arm, N > 1: D4 row-sharded (headline), D2 replicas (extras)
 # ---------------------------------------------------------------------------
-def cpu_baseline(prob, budget_s=15.0):
-    """Bounded kernel-mix sample of the reference's CPU path (oracle port),
-    scaled by the reference's call counts for this solve."""
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
-    from oracle import otn_oracle as orc
+def run_sharded(args, rank, world, dev):
+    import torch
 
-    with open(CALLMIX) as fh:
-        mix = json.load(fh)
-    calls = mix["calls"]
-    n = prob.n
-    tally = orc.Tally()
-    gamma = WORKLOAD["gamma_f"] / 8.0
-    K = -gamma * prob.C
-    rng = np.random.default_rng(0)
-    u = np.log(prob.r) + 0.01 * rng.standard_normal(n)
-    v = np.log(prob.c) + 0.01 * rng.standard_normal(n)
-    st = orc.Dual(prob.C, gamma, u, v, prob.r, prob.c, tally)
-    P = orc.tiled_plan(K, u, v)
-    x = rng.standard_normal(n)
-    w = 1.0 / np.exp(st.log_c)
-
-    def timeit(fn, reps):
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            fn()
-        return (time.perf_counter() - t0) / reps
-
-    scale = budget_s / 15.0
-    per = {
-        "lse": timeit(lambda: orc.tiled_row_lse(K, u, v), max(2, int(12 * scale))),
-        "plan": timeit(lambda: orc.tiled_plan(K, u, v, out=P), max(1, int(5 * scale))),
-        "sqmv": timeit(lambda: orc.tiled_square_mv(P, w), max(1, int(5 * scale))),
-        "mv": timeit(lambda: orc.mv(P, x, tally), max(10, int(400 * scale))),
-        "rmv": timeit(lambda: orc.rmv(P, x, tally), max(10, int(400 * scale))),
-        "round": timeit(lambda: orc.round_to_polytope(P, prob.r, prob.c, tally), 1),
-    }
-    est = sum(calls.get(k, 0) * per[k] for k in per)
-    return {"value": est, "unit": "s", "cores": os.cpu_count(), "kind": "port",
-            "sample": ("oracle port (bit-exact to the reference), OpenBLAS with all host "
-                       "threads: per-call times of each dense primitive on this n=4096 "
-                       "problem, scaled by the reference's call counts for the D2 L2^2 s0 "
-                       f"solve {calls}"),
-            "per_call_s": per,
-            "reference_full_solve_s_build_container": mix.get("oracle_wall_s")}
-
-
-def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU path (the oracle port) on the host."""
-    from paper_2504_02067_b200 import problems
-    prob = problems.workload(WORKLOAD["spec"].format(seed=0))
-    budget = max(2.0, min(args.cpu_budget, 8.0))
-    vals = []
-    for _ in range(args.warmup):
-        cpu_baseline(prob, budget_s=2.0)
-    for _ in range(args.steps):
-        vals.append(cpu_baseline(prob, budget_s=budget))
-    v = statistics.mean(x["value"] for x in vals)
-    cb = dict(vals[-1])
-    cb["value"] = v
+    import paper_2504_02067_b200 as ot
+    from paper_2504_02067_b200._device import TELEMETRY
+    from paper_2504_02067_b200.pointcloud import Comm, PointCloudCost
+    comm = Comm()
+    n = args.d4_n or 65536
+    out_extras = {}
+    # the 1-GPU reference solve of the same n on rank 0 (strong-scaling basis)
+    if rank == 0 and not args.no_extras:
+        dt1, rec1 = d4_solve(dev, n, comm=Comm.local())
+        rec1["s"] = dt1
+        out_extras["d4_1gpu"] = rec1
+    comm.barrier()
+    for _ in range(min(args.warmup, 1)):                  # a D4 solve is seconds: one warm-up
+        d4_solve(dev, n, comm)
+    times, rec = [], None
+    with ClockSampler(dev.index) as clocks:
+        for _ in range(args.steps):
+            dt, rec = d4_solve(dev, n, comm)
+            times.append(max_over_ranks(dt, world))
+    TELEMETRY.reset()
+    # e2e: the same public call with the points built on the host inside the
+    # timed region (H2D of the row shard + all column points; D2H of the result)
+    comm.barrier()
+    t0 = time.perf_counter()
+    pc = ot.points_problem(n, 3, 0)
+    sol = ot.mdot(pc, D4_GAMMA[0], D4_GAMMA[1], cost=PointCloudCost(pc, dev, comm=comm))
+    _ = sol.primal_cost
+    torch.cuda.synchronize()
+    e2e = max_over_ranks(time.perf_counter() - t0, world)
+    h2d = TELEMETRY.h2d
+    if not args.no_extras:
+        out_extras["d2_replicas"] = d2_replicas(dev, rank, world)
+    val = statistics.mean(times)
     return {
-        "metric": METRIC, "value": v, "unit": "s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded 64x64 grid cost + smooth-random marginals)",
-        "config": {"workload": "D2 n=4096 grid64 L2^2 seed=0 gamma 2^5->2^16 to 1e-6",
-                   "n": prob.n},
-        "impl": "reference",
+        "metric": METRIC_D4, "value": val, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": val * 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded U[0,1)^3 point clouds, uniform marginals)",
+        "config": config_d4(n, world),
+        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": 8},
+        "gpu_launches": None,
+        "solve": rec, "per_step_s": times, "clocks": clocks.summary(),
+        "extras": out_extras,
+    }
+
+
+def d2_replicas(dev, rank, world):
+    """D2 on every rank independently (each its own seed)."""
+    import torch
+
+    import paper_2504_02067_b200 as ot
+    p = ot.workload(f"grid:64:l2sq:{rank}")
+    dp = ot.Problem(C=torch.from_numpy(p.C).to(dev), r=p.r, c=p.c)
+    ot.mdot(dp, D2["gamma_i"], D2["gamma_f"])
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    ot.mdot(dp, D2["gamma_i"], D2["gamma_f"])
+    torch.cuda.synchronize()
+    dt = max_over_ranks(time.perf_counter() - t0, world)
+    return {"s_per_solve_max_over_ranks": dt, "solves_per_s_total": world / dt}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port, complete solves
+# ---------------------------------------------------------------------------
+def oracle_full_solves(max_solves, budget_s):
+    """Complete solves of the D2 workload by the oracle port of otnewton.mdot
+    (bit-identical to the reference), BLAS threads and the oracle's row slabs on
+    all host cores.  Runs solves until `max_solves` or until `budget_s` of
+    solving has elapsed (at least one).  Returns (seconds per solve, count,
+    cores, details)."""
+    cores = os.cpu_count() or 1
+    from oracle import otn_oracle as orc
+    from paper_2504_02067_b200 import problems
+    orc.set_threads(cores)
+    d1 = problems.workload("pts:1024:2:0")
+    t0 = time.perf_counter()
+    orc.mdot(d1.C, d1.r, d1.c, 2.0 ** 10, 2.0 ** 10)      # warm-up: BLAS / page-in (untimed)
+    warm_s = time.perf_counter() - t0
+    prob = problems.workload(D2["spec"])
+    times, run = [], None
+    while len(times) < max(1, max_solves):
+        t0 = time.perf_counter()
+        run = orc.mdot(prob.C, prob.r, prob.c, D2["gamma_i"], D2["gamma_f"], p=D2["p"],
+                       q_init=D2["q_init"])
+        times.append(time.perf_counter() - t0)
+        if sum(times) >= budget_s:
+            break
+    st = run.state
+    st.r, st.c = prob.r, prob.c
+    detail = {"stages": len(run.stages), "cg_iters": sum(pr.cg_iters for *_, pr in run.stages),
+              "true_marginal_err": st.gnorm(), "per_solve_s": times,
+              "warmup_s_d1": warm_s}
+    return statistics.mean(times), len(times), cores, detail
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(budget_s):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
+    v, k, cores, detail = oracle_full_solves(1, budget_s)
+    return {"value": v, "unit": "s", "cores": cores, "kind": "port",
+            "sample": f"{k} complete D2 solve(s) of the oracle port of otnewton.mdot "
+                      "(bit-identical to the reference: tests/test_oracle_pin.py), OpenBLAS "
+                      f"and the 256-row slabs on {cores} threads; {cpu_model()}",
+            "detail": detail}
+
+
+def run_reference(args, world):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
+    if world > 1:
+        return {"impl": "reference", "unavailable":
+                "the N>1 workload is D4 (n=65536): the reference stores 4 dense n x n float64 "
+                "arrays (137 GB) and cannot run it (SURVEY 8(c))"}
+    v, k, cores, detail = oracle_full_solves(args.steps, args.ref_budget)
+    cb = {"value": v, "unit": "s", "cores": cores, "kind": "port",
+          "sample": f"{k} complete D2 solve(s) timed (oracle port of otnewton.mdot, "
+                    "bit-identical to the reference), OpenBLAS and 256-row slabs on "
+                    f"{cores} threads; {cpu_model()}",
+          "detail": detail}
+    return {
+        "metric": METRIC, "value": v, "unit": "s", "n_gpus": world, "steps": k,
+        "warmup": 1, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded 64x64 grid cost + smooth-random marginals, reference generators)",
+        "config": dict(CONFIG_D2), "impl": "reference",
+        "steps_requested": args.steps, "warmup_note": "one untimed n=1024 solve",
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -465,10 +606,8 @@ def init_dist(args):
     if world > 1 and args.impl != "reference":
         import torch
         import torch.distributed as dist
-        backend = "gloo" if args.impl == "reference" else "nccl"
-        if backend == "nccl":
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group(backend)
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
         _PG = dist
     return rank, world
 
@@ -481,11 +620,27 @@ def barrier(world):
 def max_over_ranks(x, world):
     if world > 1 and _PG is not None:
         import torch
-        t = torch.tensor([x], dtype=torch.float64,
-                         device="cuda" if _PG.get_backend() == "nccl" else "cpu")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
         _PG.all_reduce(t, op=_PG.ReduceOp.MAX)
         return float(t.item())
     return x
+
+
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) without torchrun: re-execute this
+    script with one rank per GPU (NCCL over NVLink), rendezvous on 127.0.0.1."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -494,20 +649,33 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget", type=float, default=30.0,
+                    help="seconds of oracle solving for cpu_baseline (at least one solve)")
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="--impl reference: stop after this many seconds of solves")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--d4-n", type=int, default=65536)
-    ap.add_argument("--d4-warmup", type=int, default=0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     rank, world = init_dist(args)
     if args.impl == "reference":
-        if rank != 0:
-            return
-        out = run_reference(args, rank, world)
+        if rank == 0:
+            print(json.dumps(run_reference(args, world)))
+        return
+    import torch
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    if world == 1:
+        out = run_d2(args, dev)
+        if not args.no_extras:
+            out["extras"] = run_extras(args, dev)
+        if not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(args.cpu_budget)
     else:
-        out = run_ours(args, rank, world)
+        out = run_sharded(args, rank, world, dev)
     if rank == 0:
         print(json.dumps(out))
     if world > 1 and _PG is not None:

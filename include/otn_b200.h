@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define OTN_ABI_VERSION 1
+#define OTN_ABI_VERSION 2
 
 enum otn_status {
   OTN_OK = 0,
@@ -81,7 +81,8 @@ enum otn_reduce_op {
   OTN_RED_L1_ADD = 5,    /* [sum |a + b|]                     newton.py:199-200            */
   OTN_RED_NONPOS = 6,    /* [count(a <= 0)]                   newton.py:138                */
   OTN_RED_MAX = 7,       /* [max a]                                                        */
-  OTN_RED_L1_DOT = 8     /* [sum |a|, sum a*b]                newton.py:162-165            */
+  OTN_RED_L1_DOT = 8,    /* [sum |a|, sum a*b]                newton.py:162-165            */
+  OTN_RED_OUTSIDE = 9    /* [count(!(2^-700 <= a <= 2^700))]  shifted column-LSE check     */
 };
 
 /* Point-cloud pass operations for otn_pc_pass. */
@@ -92,7 +93,9 @@ enum otn_pc_op {
   OTN_PC_MAXD = 3,  /* out_i = max_j D_ij (raw squared distance; pass cmax = 0)             */
   OTN_PC_LSE_PART = 4, /* out_i = max_j e_ij, out2_i = sum_j exp(e_ij - out_i) (shard partial) */
   OTN_PC_DOTC = 5,  /* out_i = sum_j exp(e_ij) C_ij vec_j   (primal cost <P, C>)            */
-  OTN_PC_CDOT = 6   /* out_i = sum_j C_ij vec_j             (rank-one term of <P, C>)       */
+  OTN_PC_CDOT = 6,  /* out_i = sum_j C_ij vec_j             (rank-one term of <P, C>)       */
+  OTN_PC_LSE_SHIFT = 7 /* out_i = sum_j exp(e_ij - outer_i)  (shard partial against a known
+                          shift: ONE sum-allreduce per sharded column LSE)                 */
 };
 
 typedef struct otn_ctx otn_ctx;
@@ -108,6 +111,12 @@ typedef struct {
   double slope;        /* newton: -(grad_u . d_u)  (projector.py:205)              */
   double diag_rho;     /* NonconvergenceError diagnostics: rho                     */
   double diag_resid;   /* NonconvergenceError diagnostics: residual_l1             */
+  int32_t plan_mode;   /* plan access of the launch: 0 streamed ring, 2 / 3 compressed
+                          rows in shared / global memory (k_partition)             */
+  int32_t plan_rows_max; /* most rows owned by one CTA                               */
+  int64_t plan_nnz;    /* nonzero plan entries (materialize's per-row counts)      */
+  int64_t plan_span;   /* entries inside the rows' nonzero 64-column segments: what
+                          the ring streams per pass (roofline bytes = 8 x this)     */
 } otn_solve_result;
 
 /* ---- context ---------------------------------------------------------- */
@@ -273,6 +282,12 @@ int otn_vec_n(otn_ctx* ctx, int64_t n, int op, double s, const double* a, const 
               const double* c, const double* d, double* out);
 int otn_reduce_n(otn_ctx* ctx, int64_t n, int op, const double* a, const double* b,
                  const double* c, const double* d, double* host_out, int* host_flags);
+/* As otn_reduce_n, the two results written stream-ordered to DEVICE memory
+ * dev_out[0..1] (no host synchronization): a row-sharded solve reduces its
+ * shard into a device buffer, allreduces the buffer (NCCL, same stream order)
+ * and reads all of a step's scalars back once.                              */
+int otn_reduce_dev(otn_ctx* ctx, int64_t n, int op, const double* a, const double* b,
+                   const double* c, const double* d, double* dev_out);
 
 /* ---- projector / driver vector work ------------------------------------- */
 int otn_vec(otn_ctx* ctx, int op, double s, const double* a, const double* b, const double* c,

@@ -23,6 +23,8 @@ Jacobi-exact direction, eps_rule / error-bound constants, ...).
 from __future__ import annotations
 
 import math
+import threading
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -97,6 +99,44 @@ class Tally:
 # ---------------------------------------------------------------------------
 # dense kernels (restate _kernels.py:22-74 and newton.py:43-56)
 # ---------------------------------------------------------------------------
+# Host threads for the 256-row slabs of the dense kernels.  Every slab is an
+# independent computation (its own max, exps, pairwise sums / dgemv), so the
+# result is bit-identical for any thread count; only bench.py's CPU baseline
+# raises it (set_threads).
+THREADS = 1
+_POOL = None
+_LOCAL = threading.local()
+
+
+def set_threads(k):
+    """Run the slabs of the dense kernels on ``k`` host threads (numpy releases
+    the GIL inside its ufunc loops and OpenBLAS calls)."""
+    global THREADS, _POOL
+    k = max(1, int(k))
+    if k != THREADS:
+        if _POOL is not None:
+            _POOL.shutdown(wait=True)
+        _POOL = ThreadPoolExecutor(max_workers=k) if k > 1 else None
+        THREADS = k
+
+
+def _slabs(rows, fn):
+    spans = [(a, min(a + TILE_ROWS, rows)) for a in range(0, rows, TILE_ROWS)]
+    if _POOL is None or len(spans) == 1:
+        for a, b in spans:
+            fn(a, b)
+    else:
+        for f in [_POOL.submit(fn, a, b) for a, b in spans]:
+            f.result()
+
+
+def _scratch(rows, cols):
+    buf = getattr(_LOCAL, "buf", None)
+    if buf is None or buf.shape[0] < rows or buf.shape[1] != cols:
+        buf = _LOCAL.buf = np.empty((rows, cols))
+    return buf[:rows]
+
+
 def tiled_row_lse(K, outer, inner):
     """outer + LSE_j(K_ij + inner_j), all -inf rows -> -inf.  (_kernels.py:22-42)
 
@@ -106,10 +146,9 @@ def tiled_row_lse(K, outer, inner):
     _hit("lse")
     rows = K.shape[0]
     res = np.empty(rows)
-    scratch = np.empty((min(TILE_ROWS, rows), K.shape[1]))
-    for a in range(0, rows, TILE_ROWS):
-        b = min(a + TILE_ROWS, rows)
-        t = scratch[: b - a]
+
+    def slab(a, b):
+        t = _scratch(b - a, K.shape[1])
         np.add(K[a:b], inner[None, :], out=t)
         mx = t.max(axis=1)
         ok = np.isfinite(mx)
@@ -119,6 +158,7 @@ def tiled_row_lse(K, outer, inner):
         with np.errstate(divide="ignore"):
             val = sh + np.log(t.sum(axis=1))
         res[a:b] = np.where(ok, val, -np.inf)
+    _slabs(rows, slab)
     return outer + res
 
 
@@ -127,15 +167,21 @@ def tiled_plan(K, u, v, out=None):
     _hit("plan")
     rows, cols = K.shape
     out = np.empty((rows, cols)) if out is None else out
-    for a in range(0, rows, TILE_ROWS):
-        b = min(a + TILE_ROWS, rows)
+    over = []
+
+    def slab(a, b):
         t = out[a:b]
         np.add(K[a:b], v[None, :], out=t)
         np.add(t, u[a:b, None], out=t)
-        if t.max() > EXP_OVERFLOW:
-            raise OracleFailure("PlanOverflowError", f"log-plan entry {t.max():.3g}")
+        m = t.max()
+        if m > EXP_OVERFLOW:
+            over.append((a, m))
+            return
         with np.errstate(under="ignore"):
             np.exp(t, out=t)
+    _slabs(rows, slab)
+    if over:
+        raise OracleFailure("PlanOverflowError", f"log-plan entry {min(over)[1]:.3g}")
     return out
 
 
@@ -144,12 +190,12 @@ def tiled_square_mv(P, w):
     _hit("sqmv")
     rows = P.shape[0]
     res = np.empty(rows)
-    scratch = np.empty((min(TILE_ROWS, rows), P.shape[1]))
-    for a in range(0, rows, TILE_ROWS):
-        b = min(a + TILE_ROWS, rows)
-        t = scratch[: b - a]
+
+    def slab(a, b):
+        t = _scratch(b - a, P.shape[1])
         np.multiply(P[a:b], P[a:b], out=t)
         res[a:b] = t @ w
+    _slabs(rows, slab)
     return res
 
 
@@ -628,10 +674,13 @@ class Run:
 
 
 def mdot(C, r, c, gamma_i, gamma_f, p=1.5, q_init=2.0, adaptive_q=True,
-         adaptive_rho0=True, zero_init=False, newton_budget=200, w_r=W_ROW, w_c=W_COL):
+         adaptive_rho0=True, zero_init=False, newton_budget=200, w_r=W_ROW, w_c=W_COL,
+         projector="newton", sinkhorn_budget=10 ** 6):
     """MDOT annealing with the truncated-Newton projector (Alg. 1).
 
-    Restates driver.py:226-343 for ``projector="newton"``.
+    Restates driver.py:226-343; ``projector="sinkhorn"`` is the baseline branch
+    (driver.py:218-223,277-279: log-domain Sinkhorn to eps_d/2, rho0 untouched,
+    delta_min = +inf so the schedule grows q).
     """
     tally = Tally()
     g, g_prev, q = min(gamma_i, gamma_f), 0.0, float(q_init)
@@ -652,9 +701,14 @@ def mdot(C, r, c, gamma_i, gamma_f, p=1.5, q_init=2.0, adaptive_q=True,
         else:
             st.gamma = g
             st.r, st.c = rs, cs
-        pr = project(st, rs, cs, eps / 2.0, rho0=rho_next, newton_budget=newton_budget,
-                     adaptive_rho0=adaptive_rho0, zero_init=zero_init)
-        rho_next = rho_restart(pr.rho_final) if adaptive_rho0 else 0.0
+        if projector == "newton":
+            pr = project(st, rs, cs, eps / 2.0, rho0=rho_next, newton_budget=newton_budget,
+                         adaptive_rho0=adaptive_rho0, zero_init=zero_init)
+            rho_next = rho_restart(pr.rho_final) if adaptive_rho0 else 0.0
+        else:
+            pr = Proj()
+            pr.sinkhorn_steps = sinkhorn_sweeps(st, rs, cs, eps / 2.0, budget=sinkhorn_budget)
+            pr.grad_norm_final = st.gnorm()
         if adaptive_q:
             q = next_q(q, pr.delta_min)
         g_next = min(q * g, gamma_f)

@@ -60,7 +60,7 @@ LAUNCHES = {
     # + row stats with the gradient
     "otn_newton_step": 9,
     "otn_vec": 1, "otn_reduce": 1, "otn_row_stats": 1, "otn_accept": 1, "otn_reduce_async": 1, "otn_round_plan": 10, "otn_pc_pass": 1,
-    "otn_vec_n": 1, "otn_reduce_n": 1,
+    "otn_vec_n": 1, "otn_reduce_n": 1, "otn_reduce_dev": 1,
 }
 
 
@@ -77,7 +77,8 @@ class Telemetry:
         self.calls = {}
         self.h2d = 0
         self.d2h = 0
-        self.coop = []        # (device ms, hvps, d_v formed, n) per timed k_coop launch
+        self.coop = []        # (device ms, hvps, d_v formed, n, plan mode, nnz, span entries,
+                              #  cg iterations) per timed k_coop launch
 
     def count(self, name, sym=False):
         k = LAUNCHES.get(name, 0)

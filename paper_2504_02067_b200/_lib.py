@@ -39,8 +39,11 @@ OTN_ST_DOMAIN = 16
  VEC_SUB, VEC_ADD, VEC_PRECOND, VEC_NEG_DIV, VEC_RESCALE, VEC_LSE_FIN, VEC_LSE_FIN_SUB,
  VEC_ROUND_SCALE, VEC_SUB_MUL, VEC_MUL, VEC_COPY) = range(19)
 (RED_ROW_STATS, RED_GRAD_L1, RED_SUM_EXP, RED_DOT, RED_L1, RED_L1_ADD, RED_NONPOS,
- RED_MAX, RED_L1_DOT) = range(9)
-PC_LSE, PC_DOT, PC_DIAG, PC_MAXD, PC_LSE_PART, PC_DOTC, PC_CDOT = range(7)
+ RED_MAX, RED_L1_DOT, RED_OUTSIDE) = range(10)
+PC_LSE, PC_DOT, PC_DIAG, PC_MAXD, PC_LSE_PART, PC_DOTC, PC_CDOT, PC_LSE_SHIFT = range(8)
+
+
+ABI_VERSION = 2                 # include/otn_b200.h OTN_ABI_VERSION
 
 
 class SolveResult(ctypes.Structure):
@@ -54,6 +57,10 @@ class SolveResult(ctypes.Structure):
         ("slope", ctypes.c_double),
         ("diag_rho", ctypes.c_double),
         ("diag_resid", ctypes.c_double),
+        ("plan_mode", ctypes.c_int32),
+        ("plan_rows_max", ctypes.c_int32),
+        ("plan_nnz", ctypes.c_int64),
+        ("plan_span", ctypes.c_int64),
     ]
 
 
@@ -100,6 +107,7 @@ SIGNATURES = {
                     _P, _P, _I, _P, _P],
     "otn_vec_n": [_P, _I64, _I, _D, _P, _P, _P, _P, _P],
     "otn_reduce_n": [_P, _I64, _I, _P, _P, _P, _P, _DP, _IP],
+    "otn_reduce_dev": [_P, _I64, _I, _P, _P, _P, _P, _P],
     "otn_vec": [_P, _I, _D, _P, _P, _P, _P, _P],
     "otn_reduce": [_P, _I, _P, _P, _P, _P, _DP, _IP],
     "otn_row_stats": [_P, _P, _P, _P, _DP, _IP],
@@ -133,6 +141,10 @@ def load():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
         fn.restype = ctypes.c_char_p if name == "otn_last_error" else ctypes.c_int
+    if lib.otn_abi_version() != ABI_VERSION:
+        _load_error = (f"{LIB_PATH} has ABI {lib.otn_abi_version()}, this package needs "
+                       f"{ABI_VERSION}: rebuild it (make -C paper_2504_02067_b200/csrc)")
+        raise DeviceError(_load_error)
     _lib = lib
     return lib
 

@@ -1,9 +1,13 @@
 // extern "C" boundary: context management and the entry points declared in
 // include/otn_b200.h.  Every function validates its arguments, launches on the
 // context's stream, and returns an otn_status code.
+#include <sched.h>
+
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 
 #include "otn_internal.h"
 
@@ -40,13 +44,39 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // Wait for the stream by polling: the solver's host decisions wait on one
 // scalar after every short kernel sequence, and a blocking synchronize adds
-// the driver's wake-up latency to each of those round trips.
+// the driver's wake-up latency to each of those round trips.  The busy poll
+// is bounded: after 2 ms the thread yields between polls, after 20 ms it
+// sleeps 100 us between polls (on-the-fly passes run for seconds; one core
+// per rank must not spin for all of it).
 cudaError_t stream_wait(cudaStream_t s) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   cudaError_t e;
   while ((e = cudaStreamQuery(s)) == cudaErrorNotReady) {
+    const auto waited = clk::now() - t0;
+    if (waited > std::chrono::milliseconds(20))
+      std::this_thread::sleep_for(std::chrono::microseconds(100));
+    else if (waited > std::chrono::milliseconds(2))
+      sched_yield();
   }
   return e;
 }
+
+// The library links the static CUDA runtime, whose current device is per
+// host thread and separate from torch's: every entry point that launches
+// makes its context's device current for the call and restores the caller's.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const otn_ctx* x) {
+    int cur = -1;
+    if (x && cudaGetDevice(&cur) == cudaSuccess && cur != x->device) {
+      if (cudaSetDevice(x->device) == cudaSuccess) prev = cur;
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 int sync_copy(otn_ctx* x, void* host, const void* dev, size_t bytes, const char* what) {
   OTN_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, x->stream), what);
@@ -149,7 +179,9 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
   size_t o_sc = off; off += align_up(64 * sizeof(double), 256);
   size_t o_fl = off; off += align_up(16 * sizeof(int), 256);
   size_t o_res = off; off += align_up(sizeof(otn::DevResult), 256);
-  size_t o_part = off; off += align_up(size_t(x->coop_blocks + 2) * sizeof(int), 256);
+  // part: G + 1 row boundaries, the plan mode, then 4 ints of plan statistics
+  // (nnz and span as int64 pairs, k_partition)
+  size_t o_part = off; off += align_up(size_t(x->coop_blocks + 8) * sizeof(int), 256);
   x->ws_bytes = off;
   e = cudaMalloc(&x->ws, off);
   if (e != cudaSuccess) { delete x; return fail(OTN_ERR_CUDA, "otn_create: cudaMalloc", e); }
@@ -191,6 +223,7 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
 }
 
 int otn_destroy(otn_ctx* x) {
+  DeviceGuard dg_(x);
   if (!x) return OTN_OK;
   if (x->ws) cudaFree(x->ws);
   if (x->sg) cudaFree(x->sg);
@@ -219,6 +252,7 @@ int otn_info(const otn_ctx* x, int64_t* out4) {
 }
 
 int otn_copy(otn_ctx* x, double* dst, const double* src, int64_t n) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && dst && src && n >= 0, "otn_copy: bad argument");
   OTN_CUDA(cudaMemcpyAsync(dst, src, size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice,
                            x->stream), "otn_copy");
@@ -226,6 +260,7 @@ int otn_copy(otn_ctx* x, double* dst, const double* src, int64_t n) {
 }
 
 int otn_upload(otn_ctx* x, double* dst, const double* host_src, int64_t n) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && dst && host_src && n >= 0, "otn_upload: bad argument");
   OTN_CUDA(cudaMemcpyAsync(dst, host_src, size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
                            x->stream), "otn_upload");
@@ -233,17 +268,20 @@ int otn_upload(otn_ctx* x, double* dst, const double* host_src, int64_t n) {
 }
 
 int otn_coop_layout(otn_ctx* x, int* host) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && host, "otn_coop_layout: NULL argument");
   return sync_copy(x, host, x->part, size_t(x->coop_blocks + 2) * sizeof(int), "otn_coop_layout");
 }
 
 int otn_set_timing(otn_ctx* x, int on) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x, "otn_set_timing: NULL context");
   x->time_coop = on != 0;
   return OTN_OK;
 }
 
 int otn_coop_ms(otn_ctx* x, float* ms) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && ms, "otn_coop_ms: NULL argument");
   OTN_REQUIRE(x->time_coop, "otn_coop_ms: timing is off (otn_set_timing)");
   OTN_CUDA(cudaEventSynchronize(x->ev_coop[1]), "otn_coop_ms: sync");
@@ -252,6 +290,7 @@ int otn_coop_ms(otn_ctx* x, float* ms) {
 }
 
 int otn_read_flags(otn_ctx* x, int* host4) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && host4, "otn_read_flags: NULL argument");
   int rc = sync_copy(x, x->h_flags, x->flags, 4 * sizeof(int), "otn_read_flags");
   if (rc) return rc;
@@ -262,6 +301,7 @@ int otn_read_flags(otn_ctx* x, int* host4) {
 // ---- log-domain reductions -----------------------------------------------
 int otn_lse_rows(otn_ctx* x, const double* C, double ng, const double* outer, const double* inner,
                  double* out) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && C && inner && out, "otn_lse_rows: NULL argument");
   OTN_CUDA(otn::launch_lse_rows(x, C, ng, outer, nullptr, inner, nullptr, 0.0, 0, out),
            "otn_lse_rows");
@@ -271,6 +311,7 @@ int otn_lse_rows(otn_ctx* x, const double* C, double ng, const double* outer, co
 static int lse_cols_any(otn_ctx* x, const double* C, int sym, double ng, const double* outer,
                         const double* outer_d, const double* inner, const double* inner_d,
                         double alpha, int mode, double* out, const char* what) {
+  DeviceGuard dg_(x);
   cudaError_t e = sym ? otn::launch_lse_rows(x, C, ng, outer, outer_d, inner, inner_d, alpha, mode, out)
                       : otn::launch_lse_cols(x, C, ng, outer, outer_d, inner, inner_d, alpha, mode, out);
   OTN_CUDA(e, what);
@@ -279,12 +320,14 @@ static int lse_cols_any(otn_ctx* x, const double* C, int sym, double ng, const d
 
 int otn_lse_cols(otn_ctx* x, const double* C, int sym, double ng, const double* outer,
                  const double* inner, double* out) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && C && inner && out, "otn_lse_cols: NULL argument");
   return lse_cols_any(x, C, sym, ng, outer, nullptr, inner, nullptr, 0.0, 0, out, "otn_lse_cols");
 }
 
 int otn_rebalance_cols(otn_ctx* x, const double* C, int sym, double ng, const double* log_c,
                        const double* u, double* v_out) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && C && log_c && u && v_out, "otn_rebalance_cols: NULL argument");
   return lse_cols_any(x, C, sym, ng, log_c, nullptr, u, nullptr, 0.0, 1, v_out,
                       "otn_rebalance_cols");
@@ -293,6 +336,7 @@ int otn_rebalance_cols(otn_ctx* x, const double* C, int sym, double ng, const do
 int otn_trial_cols(otn_ctx* x, const double* C, int sym, double ng, const double* u,
                    const double* du, const double* v, const double* dv, double alpha, double* out,
                    double* host_mass) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && C && u && du && v && dv && out, "otn_trial_cols: NULL argument");
   int rc = lse_cols_any(x, C, sym, ng, v, dv, u, du, alpha, 0, out, "otn_trial_cols");
   if (rc) return rc;
@@ -311,6 +355,7 @@ int otn_trial_cols(otn_ctx* x, const double* C, int sym, double ng, const double
 int otn_materialize(otn_ctx* x, const double* C, double ng, const double* u, const double* v,
                     double* P, const double* icP, const double* rP, double* mu, int* host_overflow,
                     uint64_t* seg_mask) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && C && u && v && P, "otn_materialize: NULL argument");
   OTN_REQUIRE(!icP || (rP && mu), "otn_materialize: icP needs rP and mu");
   OTN_CUDA(cudaMemsetAsync(x->flags + 0, 0, sizeof(int), x->stream), "otn_materialize: flag");
@@ -326,13 +371,19 @@ int otn_materialize(otn_ctx* x, const double* C, double ng, const double* u, con
 }
 
 int otn_plan_mask(otn_ctx* x, const double* P, uint64_t* seg_mask) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && P && seg_mask, "otn_plan_mask: NULL argument");
+  // a system built from caller arrays (not from a materialized state) must not
+  // inherit the overflow / nonpositive-sum flags of an earlier solve on this
+  // context: the persistent solver checks flags[0..1] first
+  OTN_CUDA(cudaMemsetAsync(x->flags, 0, 2 * sizeof(int), x->stream), "otn_plan_mask: flags");
   OTN_CUDA(otn::launch_plan_mask(x, P, seg_mask), "otn_plan_mask");
   return OTN_OK;
 }
 
 int otn_system_prep(otn_ctx* x, const double* lr, const double* lc, double* rP, double* cP,
                     double* icP, int* host_bad) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && lr && lc && rP && cP && icP, "otn_system_prep: NULL argument");
   OTN_CUDA(cudaMemsetAsync(x->flags + 1, 0, sizeof(int), x->stream), "otn_system_prep: flag");
   OTN_CUDA(otn::launch_sys_prep(x, lr, lc, rP, cP, icP, x->flags + 1), "otn_system_prep");
@@ -346,6 +397,7 @@ int otn_system_prep(otn_ctx* x, const double* lr, const double* lc, double* rP, 
 }
 
 int otn_square_matvec(otn_ctx* x, const double* P, const double* w, double* out) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && P && w && out, "otn_square_matvec: NULL argument");
   OTN_CUDA(otn::launch_square_matvec(x, P, w, out), "otn_square_matvec");
   return OTN_OK;
@@ -362,6 +414,7 @@ static otn::CoopArgs plan_args(otn_ctx* x, const double* P, const uint64_t* seg_
 static int coop_op(otn_ctx* x, int mode, const double* P, const uint64_t* seg_mask,
                    const double* rP, const double* cP, double rho, const double* xin, double* out,
                    const char* what) {
+  DeviceGuard dg_(x);
   otn::CoopArgs a = plan_args(x, P, seg_mask);
   a.mode = mode;
   a.rP = rP;
@@ -374,23 +427,27 @@ static int coop_op(otn_ctx* x, int mode, const double* P, const uint64_t* seg_ma
 }
 
 int otn_matvec(otn_ctx* x, const double* P, const uint64_t* m, const double* v, double* out) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && P && v && out, "otn_matvec: NULL argument");
   return coop_op(x, otn::kModeMatvec, P, m, nullptr, nullptr, 0.0, v, out, "otn_matvec");
 }
 
 int otn_rmatvec(otn_ctx* x, const double* P, const uint64_t* m, const double* v, double* out) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && P && v && out, "otn_rmatvec: NULL argument");
   return coop_op(x, otn::kModeRmatvec, P, m, nullptr, nullptr, 0.0, v, out, "otn_rmatvec");
 }
 
 int otn_apply_F(otn_ctx* x, const double* P, const uint64_t* m, const double* rP,
                 const double* cP, double rho, const double* d, double* out) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && P && rP && cP && d && out, "otn_apply_F: NULL argument");
   return coop_op(x, otn::kModeHvp, P, m, rP, cP, rho, d, out, "otn_apply_F");
 }
 
 int otn_apply_pc(otn_ctx* x, const double* P, const uint64_t* m, const double* cP,
                  const double* d, double* out) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && P && cP && d && out, "otn_apply_pc: NULL argument");
   return coop_op(x, otn::kModePc, P, m, nullptr, cP, 0.0, d, out, "otn_apply_pc");
 }
@@ -399,6 +456,7 @@ int otn_apply_pc(otn_ctx* x, const double* P, const uint64_t* m, const double* c
 int otn_pcg(otn_ctx* x, const double* P, const uint64_t* m, const double* rP, const double* cP,
             const double* mu, double rho, const double* b, double tol, double* xv, int has_x0,
             int64_t max_iters, otn_solve_result* host_res) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && P && rP && cP && mu && b && xv, "otn_pcg: NULL argument");
   OTN_REQUIRE(max_iters >= 0, "otn_pcg: max_iters < 0");
   otn::CoopArgs a = plan_args(x, P, m);
@@ -419,6 +477,7 @@ int otn_pcg(otn_ctx* x, const double* P, const uint64_t* m, const double* rP, co
 int otn_newton(otn_ctx* x, const double* P, const uint64_t* m, const double* rP, const double* cP,
                const double* mu, const double* g, double eta, double rho0, int zero_init,
                int64_t max_iters, double* d_u, double* d_v, otn_solve_result* host_res) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && P && rP && cP && mu && g && d_u, "otn_newton: NULL argument");
   OTN_REQUIRE(max_iters >= 0, "otn_newton: max_iters < 0");
   otn::CoopArgs a = plan_args(x, P, m);
@@ -446,6 +505,7 @@ int otn_newton_step(otn_ctx* x, const double* P, const uint64_t* m, const double
                     double* trial, double* lc, double* lr, double* grad, double armijo_c1,
                     double slope_floor, otn_solve_result* host_res, double* host_out,
                     int* host_flags) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && P && rP && cP && mu && g && d_u && d_v && C && Ccols && u && v && r && log_c &&
                   trial &&
                   lc && lr && grad && host_out,
@@ -503,6 +563,7 @@ int otn_newton_step(otn_ctx* x, const double* P, const uint64_t* m, const double
 
 int otn_probe(otn_ctx* x, const double* P, const uint64_t* m, const double* cP, const double* rP,
               const double* xin, double* out, int what, int64_t reps) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && P && cP && rP && xin && out, "otn_probe: NULL argument");
   otn::CoopArgs a = plan_args(x, P, m);
   a.mode = otn::kModeProbe;
@@ -522,10 +583,12 @@ int otn_pc_pass(otn_ctx* x, int op, const double* A, int64_t na, int64_t lda, co
                 const double* colpot, const double* colpot_d, double alpha, const double* rowpot,
                 const double* vec, const double* outer, const double* outer_d, int mode,
                 double* out, double* out2) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && A && B && out, "otn_pc_pass: NULL argument");
   OTN_REQUIRE(d >= 1 && d <= 4, "otn_pc_pass: point dimension must be 1..4");
   OTN_REQUIRE(na >= 1 && nb >= 1 && lda >= na && ldb >= nb, "otn_pc_pass: bad sizes");
-  OTN_REQUIRE(op >= OTN_PC_LSE && op <= OTN_PC_CDOT, "otn_pc_pass: bad op");
+  OTN_REQUIRE(op >= OTN_PC_LSE && op <= OTN_PC_LSE_SHIFT, "otn_pc_pass: bad op");
+  OTN_REQUIRE(op != OTN_PC_LSE_SHIFT || outer != nullptr, "otn_pc_pass: LSE_SHIFT needs outer");
   OTN_REQUIRE((op != OTN_PC_DOT && op != OTN_PC_DIAG && op != OTN_PC_DOTC && op != OTN_PC_CDOT) ||
                   vec != nullptr, "otn_pc_pass: DOT/DIAG/DOTC/CDOT need vec");
   OTN_REQUIRE(op != OTN_PC_LSE_PART || out2 != nullptr, "otn_pc_pass: LSE_PART needs out2");
@@ -537,6 +600,7 @@ int otn_pc_pass(otn_ctx* x, int op, const double* A, int64_t na, int64_t lda, co
 
 int otn_vec_n(otn_ctx* x, int64_t n, int op, double s, const double* a, const double* b,
               const double* c, const double* d, double* out) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && a && out && n >= 0, "otn_vec_n: bad argument");
   OTN_REQUIRE(op >= OTN_VEC_ADD_SUB && op <= OTN_VEC_COPY, "otn_vec_n: bad op");
   if (n == 0) return OTN_OK;
@@ -546,8 +610,9 @@ int otn_vec_n(otn_ctx* x, int64_t n, int op, double s, const double* a, const do
 
 int otn_reduce_n(otn_ctx* x, int64_t n, int op, const double* a, const double* b, const double* c,
                  const double* d, double* host_out, int* host_flags) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && a && host_out && n >= 0, "otn_reduce_n: bad argument");
-  OTN_REQUIRE(op >= OTN_RED_ROW_STATS && op <= OTN_RED_L1_DOT, "otn_reduce_n: bad op");
+  OTN_REQUIRE(op >= OTN_RED_ROW_STATS && op <= OTN_RED_OUTSIDE, "otn_reduce_n: bad op");
   OTN_CUDA(cudaMemsetAsync(x->flags + 2, 0, sizeof(int), x->stream), "otn_reduce_n: flag");
   OTN_CUDA(otn::launch_reduce(x, op, n, a, b, c, d, x->scal + 8, x->flags + 2), "otn_reduce_n");
   OTN_CUDA(cudaMemcpyAsync(x->h_scal + 8, x->scal + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost,
@@ -561,9 +626,20 @@ int otn_reduce_n(otn_ctx* x, int64_t n, int op, const double* a, const double* b
   return OTN_OK;
 }
 
+int otn_reduce_dev(otn_ctx* x, int64_t n, int op, const double* a, const double* b,
+                   const double* c, const double* d, double* dev_out) {
+  DeviceGuard dg_(x);
+  OTN_REQUIRE(x && a && dev_out && n >= 0, "otn_reduce_dev: bad argument");
+  OTN_REQUIRE(op >= OTN_RED_SUM_EXP && op <= OTN_RED_OUTSIDE && op != OTN_RED_MAX,
+              "otn_reduce_dev: bad op (sums only)");
+  OTN_CUDA(otn::launch_reduce(x, op, n, a, b, c, d, dev_out, x->flags + 2), "otn_reduce_dev");
+  return OTN_OK;
+}
+
 // ---- vector work -----------------------------------------------------------
 int otn_vec(otn_ctx* x, int op, double s, const double* a, const double* b, const double* c,
             const double* d, double* out) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && a && out, "otn_vec: NULL argument");
   OTN_REQUIRE(op >= OTN_VEC_ADD_SUB && op <= OTN_VEC_COPY, "otn_vec: bad op");
   OTN_CUDA(otn::launch_vec(x, op, x->n, s, a, b, c, d, out), "otn_vec");
@@ -572,6 +648,7 @@ int otn_vec(otn_ctx* x, int op, double s, const double* a, const double* b, cons
 
 int otn_reduce_async(otn_ctx* x, int op, const double* a, const double* b, const double* c,
                      const double* d, double* host_out) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && a && host_out, "otn_reduce_async: NULL argument");
   OTN_REQUIRE(op >= OTN_RED_ROW_STATS && op <= OTN_RED_L1_DOT, "otn_reduce_async: bad op");
   // own scalar slot (40..41) and flag word (9): later reductions cannot
@@ -585,6 +662,7 @@ int otn_reduce_async(otn_ctx* x, int op, const double* a, const double* b, const
 
 int otn_row_stats(otn_ctx* x, const double* lr, const double* r, double* g, double* host_out,
                   int* host_flags) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && lr && r && g && host_out, "otn_row_stats: NULL argument");
   OTN_CUDA(cudaMemsetAsync(x->flags + 2, 0, sizeof(int), x->stream), "otn_row_stats: flag");
   OTN_CUDA(otn::launch_reduce(x, otn::kRedRowStatsGrad, x->n, lr, r, g, nullptr, x->scal + 8,
@@ -603,6 +681,7 @@ int otn_row_stats(otn_ctx* x, const double* lr, const double* r, double* g, doub
 
 int otn_accept(otn_ctx* x, double alpha, double* u, const double* d_u, double* v,
                const double* d_v, const double* log_c, const double* trial, double* lc) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && u && d_u && v && d_v && log_c && trial && lc, "otn_accept: NULL argument");
   OTN_CUDA(otn::launch_accept(x, alpha, u, d_u, v, d_v, log_c, trial, lc, nullptr), "otn_accept");
   return OTN_OK;
@@ -610,6 +689,7 @@ int otn_accept(otn_ctx* x, double alpha, double* u, const double* d_u, double* v
 
 int otn_reduce(otn_ctx* x, int op, const double* a, const double* b, const double* c,
                const double* d, double* host_out, int* host_flags) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && a && host_out, "otn_reduce: NULL argument");
   OTN_REQUIRE(op >= OTN_RED_ROW_STATS && op <= OTN_RED_L1_DOT, "otn_reduce: bad op");
   OTN_CUDA(cudaMemsetAsync(x->flags + 2, 0, sizeof(int), x->stream), "otn_reduce: flag");
@@ -627,6 +707,7 @@ int otn_reduce(otn_ctx* x, int op, const double* a, const double* b, const doubl
 
 int otn_round_plan(otn_ctx* x, double* P, const double* C, const double* r, const double* c,
                    double* host_out, int* host_flags) {
+  DeviceGuard dg_(x);
   OTN_REQUIRE(x && P && r && c && host_out, "otn_round_plan: NULL argument");
   OTN_CUDA(cudaMemsetAsync(x->flags + 3, 0, sizeof(int), x->stream), "otn_round_plan: flag");
   OTN_CUDA(otn::launch_round(x, P, C, r, c, x->scal + 16, x->flags + 3), "otn_round_plan");

@@ -1314,7 +1314,16 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
     if (row.own) a.d[row.i] = sh.sv[threadIdx.x];
   }
   res.hvps = nh;
-  if (blockIdx.x == 0 && threadIdx.x == 0) publish_result(a, res);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t* st = reinterpret_cast<const int64_t*>(a.part + ((G + 2 + 1) & ~1));
+    res.plan_mode = s_mode;
+    res.plan_nnz = st[0];
+    res.plan_span = st[1];
+    int rmax = 0;
+    for (int b = 0; b < G; ++b) rmax = max(rmax, a.part[b + 1] - a.part[b]);
+    res.plan_rows_max = rmax;
+    publish_result(a, res);
+  }
 }
 
 static_assert(kRingBytes == size_t(kRingDepth) * kSlotBytes, "ring layout");
@@ -1358,11 +1367,25 @@ __global__ void __launch_bounds__(kPartThreads) k_partition(const uint64_t* mask
   int mode = kPlanRing;
   bool sparse = false;
   int64_t s_nz = 0;                                  // nonzeros of the plan (all threads)
+  int64_t span = n * ld;                             // entries the ring streams per pass
   if (mask) {
-    int64_t nz = 0;
-    for (int64_t i = t; i < n; i += kPartThreads) nz += int64_t(__ldg(mask + i * mw + mw - 1));
+    int64_t nz = 0, sp = 0;
+    const int nt = int((ld + TILE - 1) / TILE);
+    for (int64_t i = t; i < n; i += kPartThreads) {
+      nz += int64_t(__ldg(mask + i * mw + mw - 1));
+      for (int ti = 0; ti < nt; ++ti) {               // [first, last] nonzero segment per tile
+        const uint64_t bits = __ldg(mask + i * mw + ti);
+        if (!bits) continue;
+        const int width = int(ld - int64_t(ti) * TILE < TILE ? ld - int64_t(ti) * TILE : TILE);
+        const int lo = (__ffsll(static_cast<long long>(bits)) - 1) * kSegCols;
+        const int hi = min((64 - __clzll(static_cast<long long>(bits))) * kSegCols, width);
+        sp += hi - lo;
+      }
+    }
     nz = block_sum_part<int64_t>(nz, s_buf);
+    sp = block_sum_part<int64_t>(sp, s_buf);
     s_nz = nz;
+    span = sp;
     const int64_t cap = sg_ok ? kSparseGCap : kSparseCap;
     // compressed rows pay 10 B per nonzero per pass (value + column) against
     // 8 B per span column: only below half density
@@ -1424,6 +1447,11 @@ __global__ void __launch_bounds__(kPartThreads) k_partition(const uint64_t* mask
     if (sparse) mode = no_smem == 0 ? kPlanSparse : kPlanSparseG;
   }
   __syncthreads();
+  if (t == 0) {                                      // statistics for the launch record
+    int64_t* st = reinterpret_cast<int64_t*>(part + ((G + 2 + 1) & ~1));
+    st[0] = mask ? s_nz : n * ld;
+    st[1] = span;
+  }
   if (sparse) {
     if (t == 0) part[G + 1] = mode;
     return;

@@ -28,6 +28,10 @@ struct DevResult {
   double slope;         // -(grad_u . d_u)  (projector.py:205)
   double diag_rho;      // NonconvergenceError diagnostics (newton.py:168-172)
   double diag_resid;
+  int32_t plan_mode;    // k_partition's choice for this launch
+  int32_t plan_rows_max;
+  int64_t plan_nnz;     // nonzeros of the plan
+  int64_t plan_span;    // entries in nonzero 64-column segments
 };
 
 }  // namespace otn

@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
     rp[r] = (p.rowpot && i < p.na) ? __ldg(p.rowpot + i) : 0.0;
     m[r] = (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART || OP == OTN_PC_MAXD || OP == OTN_PC_DIAG)
                ? OTN_NINF : 0.0;
+    if (OP == OTN_PC_LSE_SHIFT) m[r] = i < p.na ? __ldg(p.outer + i) : 0.0;   // fixed shift
     s[r] = 0.0;
   }
   for (int64_t j0 = 0; j0 < p.nb; j0 += kPcTile) {
@@ -89,7 +90,25 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
     }
     __syncthreads();
     const int jn = int(p.nb - j0 < kPcTile ? p.nb - j0 : int64_t(kPcTile));
-    if (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART) {
+    if (OP == OTN_PC_LSE_SHIFT) {
+      // against the known shift: no running max, no rescale
+#pragma unroll
+      for (int r = 0; r < RW; ++r) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int t = lane + 32 * q;
+          if (t < jn) {
+            double bb[D];
+#pragma unroll
+            for (int k = 0; k < D; ++k) bb[k] = sb[k][t];
+            const double c = pc_cost<D>(a[r], bb, p.cmax, rc);
+            double e = __dadd_rn(__dmul_rn(p.ng, c), scp[t]);
+            if (p.rowpot) e = __dadd_rn(e, rp[r]);
+            s[r] += exp_tab(__dsub_rn(e, m[r]), s_exp);
+          }
+        }
+      }
+    } else if (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART) {
       // 8 columns per lane per tile: chunk max, one rescale, then exps
 #pragma unroll
       for (int r = 0; r < RW; ++r) {
@@ -173,6 +192,8 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
       } else if (OP == OTN_PC_LSE_PART) {
         p.out[i] = mm;
         p.out2[i] = ss;
+      } else if (OP == OTN_PC_LSE_SHIFT) {
+        p.out[i] = ss;
       } else if (OP == OTN_PC_MAXD) {
         p.out[i] = mm;
       } else {
@@ -198,7 +219,8 @@ static cudaError_t launch_rw(const PairArgs& p, cudaStream_t st) {
 // 1.6-1.8x slower).
 template <int D, int OP>
 static cudaError_t launch_d(const PairArgs& p, cudaStream_t st, int num_sms) {
-  if (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART || (p.na + 31) / 32 < num_sms)
+  if (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART || OP == OTN_PC_LSE_SHIFT ||
+      (p.na + 31) / 32 < num_sms)
     return launch_rw<2, D, OP, 3>(p, st);
   return launch_rw<4, D, OP, 2>(p, st);
 }
@@ -223,6 +245,7 @@ cudaError_t launch_pair(otn_ctx* x, const PairArgs& p) {
     case OTN_PC_LSE_PART: return launch_pair_op<OTN_PC_LSE_PART>(p, x->stream, x->num_sms);
     case OTN_PC_DOTC: return launch_pair_op<OTN_PC_DOTC>(p, x->stream, x->num_sms);
     case OTN_PC_CDOT: return launch_pair_op<OTN_PC_CDOT>(p, x->stream, x->num_sms);
+    case OTN_PC_LSE_SHIFT: return launch_pair_op<OTN_PC_LSE_SHIFT>(p, x->stream, x->num_sms);
     default: return cudaErrorInvalidValue;
   }
 }

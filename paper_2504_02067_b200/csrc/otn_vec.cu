@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(1024) k_reduce(int op, int64_t n, const double
       case OTN_RED_L1_ADD: s0 += fabs(__dadd_rn(a[i], b[i])); break;
       case OTN_RED_NONPOS: if (a[i] <= 0.0) s0 += 1.0; break;
       case OTN_RED_L1_DOT: s0 += fabs(a[i]); s1 = fma(a[i], b[i], s1); break;
+      case OTN_RED_OUTSIDE: if (!(a[i] >= 0x1p-700 && a[i] <= 0x1p+700)) s0 += 1.0; break;
       case OTN_RED_MAX: s1 = (i == threadIdx.x) ? a[i] : fmax(s1, a[i]); break;
       default: break;
     }

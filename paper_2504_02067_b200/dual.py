@@ -475,6 +475,11 @@ class DualState:
         primal = _round_device(k, P, self._dc.C, k.vec(problem.r), k.vec(problem.c))
         opcount.add(1)          # <P, C>  (driver.py:309)
         if is_tensor(problem.C):
+            # the returned plan leaves the state: a later from_state /
+            # materialize_plan(reuse_buffer=True) on final_state gets a new
+            # buffer instead of overwriting Solution.P (the reference returns
+            # a fresh array from round_plan, driver.py:178-208)
+            self._plan_buf = None
             return P[:, : problem.n], primal
         # D2H through page-locked memory (DMA at full PCIe/C2C rate; a pageable
         # copy of the 134 MB plan is ~25x slower); torch caches the pinned block

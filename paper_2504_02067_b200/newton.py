@@ -252,7 +252,9 @@ def _newton_device(grad_u, sys, eta, rho0, zero_init, max_cg_iters, d_u, d_v):
            vptr(grad_u), float(eta), float(rho0), int(bool(zero_init)), int(max_cg_iters),
            vptr(d_u), vptr(d_v), ctypes.byref(res))
     if timed:
-        TELEMETRY.coop.append((k.coop_ms(), int(res.hvps), int(d_v is not None), k.n))
+        TELEMETRY.coop.append((k.coop_ms(), int(res.hvps), int(d_v is not None), k.n,
+                               int(res.plan_mode), int(res.plan_nnz), int(res.plan_span),
+                               int(res.cg_iters)))
     if res.pcg_calls > 0:
         sys._tally_mu()
     opcount.add(2 * int(res.hvps))
@@ -291,7 +293,8 @@ def _newton_step_device(state, sys, grad_u, eta, rho0, zero_init, max_cg_iters, 
            int(max_cg_iters), *mid, state._ng, *tail,
            float(armijo_c1), float(slope_floor), ctypes.byref(res), out, ctypes.byref(fl))
     if timed:
-        TELEMETRY.coop.append((k.coop_ms(), int(res.hvps), 1, k.n))
+        TELEMETRY.coop.append((k.coop_ms(), int(res.hvps), 1, k.n, int(res.plan_mode),
+                               int(res.plan_nnz), int(res.plan_span), int(res.cg_iters)))
     if res.pcg_calls > 0:
         sys._tally_mu()
     opcount.add(2 * int(res.hvps))

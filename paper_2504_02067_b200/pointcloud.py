@@ -12,10 +12,13 @@ round trip is noise next to a pass — which also lets the solve be **row
 sharded** across GPUs: rank g owns rows [g n/G, (g+1) n/G) of X (all of Y is
 replicated, 24n bytes).  Row-direction work (row LSE, P w, the Jacobi
 diagonal, CG vector algebra) is local; every column-direction product (column
-LSE, P^T x) yields per-rank partials combined by ONE allreduce per product
-(column LSE: MAX of the shifts, then SUM of the rescaled sums), and CG dots /
-norms by an allreduce of 1-2 scalars (``Comm``).  On one GPU ``Comm`` is the
-identity.
+LSE, P^T x) yields per-rank partials combined by ONE allreduce per product:
+P^T x partials are summed; the column LSE is formed against a known shift
+(the previous column LSE, SURVEY §7 hard part 4) so its partial sums need one
+SUM allreduce too, with the MAX-then-SUM combine as the fallback when a sum
+leaves [2^-700, 2^700].  CG dots / norms are reduced into a device buffer and
+allreduced there, one host read per CG scalar step (``Comm``).  On one GPU
+``Comm`` is the identity.
 
 The state class mirrors the private hooks ``project()`` and ``mdot()`` use on
 ``DualState``, so the projector and driver are shared with the stored path.
@@ -43,9 +46,12 @@ TRUE_RESIDUAL_REFRESH = 50
 
 
 class Comm:
-    """Collectives of a row-sharded solve (torch.distributed, NCCL on GPUs).
+    """Collectives of a row-sharded solve (torch.distributed: NCCL between
+    GPUs; gloo in the CPU tests and the GPU process-group test, where CUDA
+    tensors are staged through the host).
 
-    ``world == 1`` (no process group) makes every method the identity."""
+    ``world == 1`` (no process group) makes every method the identity.
+    ``stats`` counts the collectives (vector / scalar allreduces, bytes)."""
 
     def __init__(self, group=None):
         self.group = group
@@ -56,34 +62,59 @@ class Comm:
             self.dist = None
         self.world = self.dist.get_world_size(group) if self.dist else 1
         self.rank = self.dist.get_rank(group) if self.dist else 0
+        self.backend = str(self.dist.get_backend(group)) if self.dist else None
+        self.stats = {"vector_allreduces": 0, "scalar_allreduces": 0, "bytes": 0}
+
+    @classmethod
+    def local(cls):
+        """A one-rank communicator even inside a process group (the 1-GPU
+        reference solve of a multi-rank job)."""
+        c = cls.__new__(cls)
+        c.group, c.dist, c.world, c.rank, c.backend = None, None, 1, 0, None
+        c.stats = {"vector_allreduces": 0, "scalar_allreduces": 0, "bytes": 0}
+        return c
 
     def shard(self, n):
         lo = (self.rank * n) // self.world
         hi = ((self.rank + 1) * n) // self.world
         return lo, hi
 
-    def sum_(self, t):
+    def barrier(self):
         if self.world > 1:
-            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+            self.dist.barrier(group=self.group)
+
+    def _allreduce(self, t, op, kind):
+        if self.world == 1:
+            return t
+        self.stats[kind] += 1
+        self.stats["bytes"] += t.numel() * t.element_size()
+        if self.backend == "gloo" and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, op=op, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, op=op, group=self.group)
         return t
 
+    def sum_(self, t, kind="vector_allreduces"):
+        return self._allreduce(t, self.dist.ReduceOp.SUM if self.dist else None, kind)
+
     def max_(self, t):
-        if self.world > 1:
-            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
-        return t
+        return self._allreduce(t, self.dist.ReduceOp.MAX if self.dist else None,
+                               "vector_allreduces")
 
     def sum_scalars(self, vals, device):
         if self.world == 1:
             return [float(v) for v in vals]
         t = torch().tensor(list(vals), dtype=torch().float64, device=device)
-        self.sum_(t)
+        self.sum_(t, "scalar_allreduces")
         return [float(v) for v in t.tolist()]
 
     def max_scalars(self, vals, device):
         if self.world == 1:
             return [float(v) for v in vals]
         t = torch().tensor(list(vals), dtype=torch().float64, device=device)
-        self.max_(t)
+        self._allreduce(t, self.dist.ReduceOp.MAX, "scalar_allreduces")
         return [float(v) for v in t.tolist()]
 
 
@@ -112,6 +143,11 @@ class CudaBackend:
                       ctypes.byref(fl))
         return float(out[0]), float(out[1]), int(fl.value)
 
+    def reduce_dev(self, n, op, dst, a, b=None, c=None, d=None):
+        """The two sums into device memory dst[0:2] (stream-ordered, no sync)."""
+        self.ctx.call("otn_reduce_dev", int(n), int(op), vptr(a), vptr(b), vptr(c), vptr(d),
+                      vptr(dst))
+
     def tensor(self, arr):
         TELEMETRY.h2d += arr.nbytes
         return torch().from_numpy(arr.copy()).to(self.device)
@@ -139,6 +175,8 @@ class PointCloudCost:
         self.Xt = self.be.tensor(X)
         self.Yt = self.be.tensor(Y)
         self.symmetric = bool(np.array_equal(problem.X, problem.Y))
+        self._scal_buf = None
+        self._colL = None          # last column LSE (sharded runs: the next call's shift)
         if problem.cmax is not None:
             self.cmax = float(problem.cmax)
         else:
@@ -171,6 +209,27 @@ class PointCloudCost:
     def reduce(self, n, op, a, b=None, c=None, d=None):
         return self.be.reduce(n, op, a, b, c, d)
 
+    def rsum(self, *items):
+        """Sum-reductions over ALL rows: each item (n, op, a, b, ...) is reduced
+        over this shard; on several ranks the shard sums go into one device
+        buffer, ONE allreduce combines them and one host read returns them.
+        Returns a list of (s0, s1) pairs."""
+        if self.comm.world == 1:
+            return [self.be.reduce(*it)[:2] for it in items]
+        t = torch()
+        buf = self._scal_buf
+        if buf is None or buf.numel() < 2 * len(items):
+            buf = self._scal_buf = t.zeros(max(8, 2 * len(items)), dtype=t.float64,
+                                           device=self.device)
+        for k, it in enumerate(items):
+            n, op, *vecs = it
+            vecs = list(vecs) + [None] * (4 - len(vecs))
+            self.be.reduce_dev(n, op, buf[2 * k: 2 * k + 2], *vecs)
+        view = buf[: 2 * len(items)]
+        self.comm.sum_(view, "scalar_allreduces")
+        vals = view.tolist()
+        return [(vals[2 * k], vals[2 * k + 1]) for k in range(len(items))]
+
     def zeros(self, n):
         t = torch()
         return t.zeros(n, dtype=t.float64, device=self.device)
@@ -185,21 +244,42 @@ class PointCloudCost:
             self.pass_(_lib.PC_LSE, rows_first=False, out=out, ng=ng, colpot=inner,
                        colpot_d=inner_d, alpha=alpha, outer=outer, outer_d=outer_d, mode=mode)
             return
-        m = self.zeros(self.n)
-        s = self.zeros(self.n)
-        self.pass_(_lib.PC_LSE_PART, rows_first=False, out=m, out2=s, ng=ng, colpot=inner,
-                   colpot_d=inner_d, alpha=alpha)
-        M = m.clone()
-        self.comm.max_(M)
-        self.vec(self.n, _lib.VEC_RESCALE, s, s, m, M)        # s * exp(m - M)
-        self.comm.sum_(s)
+        n = self.n
+        zero = self.zeros(n)
+        L = self.zeros(n)
+        done = False
+        self.comm.stats["column_products"] = self.comm.stats.get("column_products", 0) + 1
+        if self._colL is not None:
+            # ONE allreduce: shard sums of exp(e_ij - L_prev_j), L = L_prev + log(sum)
+            s = self.zeros(n)
+            self.pass_(_lib.PC_LSE_SHIFT, rows_first=False, out=s, ng=ng, colpot=inner,
+                       colpot_d=inner_d, alpha=alpha, outer=self._colL)
+            self.comm.sum_(s)
+            # every rank holds the same s: the same verdict everywhere
+            if self.reduce(n, _lib.RED_OUTSIDE, s)[0] == 0.0:
+                self.vec(n, _lib.VEC_LSE_FIN, L, zero, self._colL, s)
+                done = True
+            self.comm.stats["lse_shift_fallbacks"] = (
+                self.comm.stats.get("lse_shift_fallbacks", 0) + (0 if done else 1))
+        if not done:
+            # exact combine: MAX of the shard maxima, then SUM of the rescaled sums
+            m = self.zeros(n)
+            s = self.zeros(n)
+            self.pass_(_lib.PC_LSE_PART, rows_first=False, out=m, out2=s, ng=ng, colpot=inner,
+                       colpot_d=inner_d, alpha=alpha)
+            M = m.clone()
+            self.comm.max_(M)
+            self.vec(n, _lib.VEC_RESCALE, s, s, m, M)         # s * exp(m - M)
+            self.comm.sum_(s)
+            self.vec(n, _lib.VEC_LSE_FIN, L, zero, M, s)
+        self._colL = L
         base = outer
         if outer_d is not None:
-            base = self.zeros(self.n)
-            self.vec(self.n, _lib.VEC_AXPY, base, outer, outer_d, s=alpha)
+            base = self.zeros(n)
+            self.vec(n, _lib.VEC_AXPY, base, outer, outer_d, s=alpha)
         if base is None:
-            base = self.zeros(self.n)
-        self.vec(self.n, _lib.VEC_LSE_FIN if mode == 0 else _lib.VEC_LSE_FIN_SUB, out, base, M, s)
+            base = zero
+        self.vec(n, _lib.VEC_ADD if mode == 0 else _lib.VEC_SUB, out, base, L)
 
 
 class PointCloudState:
@@ -347,8 +427,10 @@ class PointCloudState:
             lr = self._lr_dev()
             pc.vec(pc.rows, _lib.VEC_GRAD, self._g, lr, self._r)
             s0, s1, fl = pc.reduce(pc.rows, _lib.RED_ROW_STATS, lr, self._r)
-            s0, s1 = pc.comm.sum_scalars([s0, s1], pc.device)
-            fl = int(pc.comm.max_scalars([fl], pc.device)[0])
+            if pc.comm.world > 1:                         # one allreduce: sums + flag counts
+                s0, s1, f1, f2 = pc.comm.sum_scalars([s0, s1, fl & 1, (fl >> 1) & 1],
+                                                     pc.device)
+                fl = (1 if f1 > 0 else 0) | (2 if f2 > 0 else 0)
             self._rowstat = (s0, s1, fl)
         return self._rowstat
 
@@ -365,17 +447,16 @@ class PointCloudState:
 
     def grad_norm_l1(self):
         pc = self._pc
-        a = pc.reduce(pc.rows, _lib.RED_GRAD_L1, self._lr_dev(), self._r, self._lc_dev(), self._c)
-        gu = pc.comm.sum_scalars([a[0]], pc.device)[0]
+        gu = pc.rsum((pc.rows, _lib.RED_GRAD_L1, self._lr_dev(), self._r, self._lc_dev(),
+                      self._c))[0][0]
         gv = pc.reduce(self.n, _lib.RED_GRAD_L1, self._lc_dev(), self._c, self._lc_dev(),
                        self._c)[0]
         return float(gu + gv)
 
     def dual_value(self):
         pc = self._pc
-        mass = pc.reduce(pc.rows, _lib.RED_SUM_EXP, self._lr_dev())[0]
-        ur = pc.reduce(pc.rows, _lib.RED_DOT, self._u, self._r)[0]
-        mass, ur = pc.comm.sum_scalars([mass, ur], pc.device)
+        (mass, _), (ur, _) = pc.rsum((pc.rows, _lib.RED_SUM_EXP, self._lr_dev()),
+                                     (pc.rows, _lib.RED_DOT, self._u, self._r))
         vc = pc.reduce(self.n, _lib.RED_DOT, self._v, self._c)[0]
         return mass - 1.0 - ur - vc
 
@@ -539,13 +620,15 @@ class PointCloudSystem:
 
     def _dot(self, a, b):
         pc = self._pc
-        return pc.comm.sum_scalars([pc.reduce(pc.rows, _lib.RED_DOT, a, b)[0]], pc.device)[0]
+        return pc.rsum((pc.rows, _lib.RED_DOT, a, b))[0][0]
 
     def _rmatvec(self, x, out):
         """out = P^T x, summed over all shards (newton.py:51-56)."""
         pc = self._pc
         pc.pass_(_lib.PC_DOT, rows_first=False, out=out, ng=self._ng, order=1, rowpot=self._v,
                  colpot=self._u, vec=x)
+        if pc.comm.world > 1:
+            pc.comm.stats["column_products"] = pc.comm.stats.get("column_products", 0) + 1
         pc.comm.sum_(out)
 
     def _hvp(self, rho, x, out, res):
@@ -571,7 +654,7 @@ class PointCloudSystem:
             self._mu_counted = True
         M = pc.zeros(nr)
         pc.vec(nr, _lib.VEC_PRECOND, M, self._rP, self._mu, s=float(rho))
-        if pc.comm.sum_scalars([pc.reduce(nr, _lib.RED_NONPOS, M)[0]], pc.device)[0] > 0:
+        if pc.rsum((nr, _lib.RED_NONPOS, M))[0][0] > 0:
             return _lib.OTN_ST_PRECOND, 0, 0.0
         r = pc.zeros(nr)
         q = pc.zeros(nr)
@@ -583,8 +666,7 @@ class PointCloudSystem:
             r.copy_(b)
         z = pc.zeros(nr)
         pc.vec(nr, _lib.VEC_DIV, z, r, M)
-        a = pc.reduce(nr, _lib.RED_L1_DOT, r, z)
-        norm, rz = pc.comm.sum_scalars([a[0], a[1]], pc.device)
+        norm, rz = pc.rsum((nr, _lib.RED_L1_DOT, r, z))[0]
         if norm <= tol:
             return _lib.OTN_OK, 0, norm
         p = z.clone()
@@ -600,8 +682,7 @@ class PointCloudSystem:
                 self._hvp(rho, x, q, res)
                 pc.vec(nr, _lib.VEC_SUB, r, b, q)
             pc.vec(nr, _lib.VEC_DIV, z, r, M)
-            a = pc.reduce(nr, _lib.RED_L1_DOT, r, z)
-            norm, rz_new = pc.comm.sum_scalars([a[0], a[1]], pc.device)
+            norm, rz_new = pc.rsum((nr, _lib.RED_L1_DOT, r, z))[0]
             if norm <= tol:
                 return _lib.OTN_OK, k, norm
             pc.vec(nr, _lib.VEC_AXPY, p, z, p, s=rz_new / rz)
@@ -615,7 +696,7 @@ class PointCloudSystem:
         res = _Result()
         if max_cg_iters is None:
             max_cg_iters = 10 * self.n
-        gn = pc.comm.sum_scalars([pc.reduce(nr, _lib.RED_L1, grad_u)[0]], pc.device)[0]
+        gn = pc.rsum((nr, _lib.RED_L1, grad_u))[0][0]
         res.rho_final = rho0
         if gn == 0.0:
             d_u.zero_()
@@ -629,8 +710,7 @@ class PointCloudSystem:
             q = pc.zeros(nr)
             while True:
                 self._hvp(1.0, d_u, q, res)
-                rn = pc.comm.sum_scalars([pc.reduce(nr, _lib.RED_L1_ADD, q, grad_u)[0]],
-                                         pc.device)[0]
+                rn = pc.rsum((nr, _lib.RED_L1_ADD, q, grad_u))[0][0]
                 if rn <= target:
                     res.resid_l1 = rn
                     break

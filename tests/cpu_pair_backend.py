@@ -39,6 +39,12 @@ class CpuPairBackend:
             cp = cp + alpha * colpot_d[:nb]
         rp = None if rowpot is None else rowpot[:na]
         kc = ng * C
+        if op == _lib.PC_LSE_SHIFT:
+            e = kc + cp[None, :]
+            if rp is not None:
+                e = e + rp[:, None]
+            out[:na] = torch.exp(e - outer[:na][:, None]).sum(dim=1)
+            return
         if op in (_lib.PC_LSE, _lib.PC_LSE_PART):
             e = kc + cp[None, :]
             if rp is not None:
@@ -125,4 +131,12 @@ class CpuPairBackend:
             return float(A.max()) if n else -np.inf, 0.0, 0
         if op == L.RED_L1_DOT:
             return float(A.abs().sum()), float(A @ b[:n]), 0
+        if op == L.RED_OUTSIDE:
+            ok = (A >= 2.0 ** -700) & (A <= 2.0 ** 700)
+            return float((~ok).sum()), 0.0, 0
         raise ValueError(op)
+
+    def reduce_dev(self, n, op, dst, a, b=None, c=None, d=None):
+        s0, s1, _ = self.reduce(n, op, a, b, c, d)
+        dst[0] = s0
+        dst[1] = s1

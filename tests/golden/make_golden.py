@@ -56,6 +56,15 @@ SMALL = [
     ("pix256_784_s0", "pix:256:784:0", 2.0 ** 5, 2.0 ** 14),
 ]
 
+# MdotOptions(projector="sinkhorn"): the log-domain Sinkhorn baseline branch
+# (driver.py:218-223,277-279 -> oracles.py:243-265), several gamma stages each
+SINKHORN = [
+    ("sk_grid16_l1_s1", "grid:16:l1:1", 2.0 ** 5, 2.0 ** 10),
+    ("sk_grid16_l2sq_s1", "grid:16:l2sq:1", 2.0 ** 5, 2.0 ** 12),
+    ("sk_pts256_2d_s0", "pts:256:2:0", 2.0 ** 5, 2.0 ** 10),
+    ("sk_pts1024_3d_s0", "pts:1024:3:0", 2.0 ** 5, 2.0 ** 9),
+]
+
 LARGE = [
     ("D2_grid64_l1_s0", "grid:64:l1:0", 2.0 ** 5, 2.0 ** 16),
     ("D2_grid64_l2sq_s0", "grid:64:l2sq:0", 2.0 ** 5, 2.0 ** 16),
@@ -116,21 +125,22 @@ def strip_ops(stages):
     return [{k: v for k, v in s.items() if k != "ops_n2"} for s in stages]
 
 
-def run_case(name, spec, gi, gf, verify_oracle):
+def run_case(name, spec, gi, gf, verify_oracle, projector="newton"):
     prob = ref_problem(spec)
+    opts = ref.MdotOptions(projector=projector)
     p2 = mine.workload(spec)
     gens_equal = (np.array_equal(prob.C, p2.C) and np.array_equal(prob.r, p2.r)
                   and np.array_equal(prob.c, p2.c))
     assert gens_equal, f"{spec}: package generators differ from the reference's"
     ref_opcount.reset()
     t0 = time.monotonic()
-    sol = ref.mdot(prob, gi, gf)
+    sol = ref.mdot(prob, gi, gf, opts=opts)
     wall = time.monotonic() - t0
     st = sol.final_state
     st.set_targets(prob.r, prob.c)
     true_err = st.grad_norm_l1()
     meta = dict(
-        name=name, spec=spec, gamma_i=gi, gamma_f=gf, n=prob.n,
+        name=name, spec=spec, gamma_i=gi, gamma_f=gf, n=prob.n, projector=projector,
         sha_C=sha(prob.C), sha_r=sha(prob.r), sha_c=sha(prob.c),
         primal=sol.primal_cost, error_bound=sol.error_bound,
         dual_value=sol.report.dual_value_final, grad_norm_final=sol.report.grad_norm_final,
@@ -149,7 +159,7 @@ def run_case(name, spec, gi, gf, verify_oracle):
     os.environ["OTN_DETERMINISTIC"] = "1"
     try:
         ref_opcount.reset()
-        det = ref.mdot(ref.Problem(C=prob.C, r=prob.r, c=prob.c), gi, gf)
+        det = ref.mdot(ref.Problem(C=prob.C, r=prob.r, c=prob.c), gi, gf, opts=opts)
     finally:
         del os.environ["OTN_DETERMINISTIC"]
     du_det = float(np.abs(det.final_state.u - st.u).max() / np.abs(st.u).max())
@@ -165,7 +175,7 @@ def run_case(name, spec, gi, gf, verify_oracle):
     if prob.n <= 64:
         arrays["P"] = sol.P.copy()
     if verify_oracle:
-        run = orc.mdot(prob.C, prob.r, prob.c, gi, gf)
+        run = orc.mdot(prob.C, prob.r, prob.c, gi, gf, projector=projector)
         same = (np.array_equal(run.state.u, st.u) and np.array_equal(run.state.v, st.v)
                 and run.primal == sol.primal_cost and run.ops == sol.report.ops
                 and oracle_trajectory(run) == strip_ops(meta["stages"]))
@@ -232,12 +242,14 @@ def main():
     ap.add_argument("--verify-oracle", action="store_true")
     args = ap.parse_args()
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
+    orc.set_threads(os.cpu_count())       # slab-parallel oracle: bit-identical results
     kernel_goldens()
-    cases = SMALL + (LARGE if args.large else [])
-    for name, spec, gi, gf in cases:
+    cases = ([c + ("newton",) for c in SMALL] + [c + ("sinkhorn",) for c in SINKHORN]
+             + ([c + ("newton",) for c in LARGE] if args.large else []))
+    for name, spec, gi, gf, projector in cases:
         if args.only and args.only not in name:
             continue
-        run_case(name, spec, gi, gf, args.verify_oracle)
+        run_case(name, spec, gi, gf, args.verify_oracle, projector)
 
 
 if __name__ == "__main__":

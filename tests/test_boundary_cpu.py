@@ -32,7 +32,7 @@ def test_library_loads_and_exports_every_symbol():
     lib = ctypes.CDLL(_lib.LIB_PATH)
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert _lib.load().otn_abi_version() == 1
+    assert _lib.load().otn_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_no_cpu_fallback_without_device():

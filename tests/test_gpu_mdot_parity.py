@@ -7,9 +7,12 @@ Gates:
             per-stage Newton-step and CG-iteration counts, identical op tallies,
             u and v within 1e-10 (inf-norm relative);
   spread  — squared-L2 grids and the 784-d pixel sets, where the reference
-            moves by up to 7 CG iterations / 4.7e-5 in u against itself
-            (BASELINE.md §2): identical stage count, CG totals within 2%,
-            u and v within 1e-4, true-marginal error <= 1e-6 at full size.
+            does not reproduce itself to 1e-9 (D2-L2^2: 789 vs
+            785 CG in stage 14, u within 3.4e-11): identical gamma schedule and
+            Newton counts, each stage's CG count within the reference's own
+            det-vs-BLAS difference for that stage (so equal wherever the
+            reference agrees with itself), u and v within 10x its self-spread,
+            primal within 1e-9 relative, true-marginal error <= 1e-6 at full size.
 """
 
 import numpy as np
@@ -54,7 +57,8 @@ def run_case(name, on_device=False):
     if on_device:
         prob = device_problem(prob)
     opcount.reset()
-    sol = mdot(prob, meta["gamma_i"], meta["gamma_f"])
+    sol = mdot(prob, meta["gamma_i"], meta["gamma_f"],
+               opts=MdotOptions(projector=meta.get("projector", "newton")))
     return meta, arr, prob, sol
 
 
@@ -77,6 +81,8 @@ def check(meta, arr, sol, name):
         assert [it.gamma for it in sol.iterations] == [s["gamma"] for s in meta["stages"]]
         assert got_newton == ref_newton, (got_newton, ref_newton)
         assert got_cg == ref_cg, (got_cg, ref_cg)
+        got_sk = [it.stats.sinkhorn_steps for it in sol.iterations]
+        assert got_sk == [s["sinkhorn_steps"] for s in meta["stages"]], got_sk
         assert sol.report.ops == meta["ops"]
         assert du <= tol and dv <= tol, (du, dv, tol)
         assert sol.primal_cost == pytest.approx(meta["primal"], rel=1e-9, abs=1e-14)
@@ -95,13 +101,24 @@ def check(meta, arr, sol, name):
         st.set_targets(sol.final_state.problem.r, sol.final_state.problem.c)
         assert st.grad_norm_l1() <= max(eps_last, 2 * meta["true_marginal_err"])
     else:
-        # inside the reference's own BLAS-vs-deterministic spread (x2, + 2%)
-        spread_cg = abs(ss.get("cg_total", sum(ref_cg)) - sum(ref_cg))
-        assert abs(sum(got_cg) - sum(ref_cg)) <= 2 * spread_cg + max(10, 0.02 * sum(ref_cg)), \
-            (got_cg, ref_cg, ss.get("cg"))
-        tol = max(1e-6, 10 * ss.get("du", 0.0), 10 * ss.get("dv", 0.0))
+        # inside the reference's own BLAS-vs-deterministic spread (BASELINE.md
+        # section 2): the same gamma schedule and Newton-step counts, every
+        # stage's CG count within that stage's det-vs-BLAS difference (0 where
+        # the reference reproduces itself), the CG total within the reference's
+        # own total difference, u and v within 10x the reference's own spread.
+        assert [it.gamma for it in sol.iterations] == [s["gamma"] for s in meta["stages"]]
+        assert got_newton == ref_newton, (got_newton, ref_newton)
+        det_cg = ss["cg"]
+        for k, (a, b, c) in enumerate(zip(got_cg, ref_cg, det_cg)):
+            assert abs(a - b) <= abs(c - b), ("stage", k, a, b, c)
+        assert abs(sum(got_cg) - sum(ref_cg)) <= abs(ss["cg_total"] - sum(ref_cg)), \
+            (sum(got_cg), sum(ref_cg), ss["cg_total"])
+        tol = max(1e-10, 10 * ss["du"], 10 * ss["dv"])
         assert du <= tol and dv <= tol, (du, dv, tol)
-        assert sol.primal_cost == pytest.approx(meta["primal"], rel=1e-6, abs=1e-12)
+        assert sol.primal_cost == pytest.approx(meta["primal"], rel=1e-9, abs=1e-14)
+    print(f"{name}: gate={g} stages={len(got_cg)} cg={sum(got_cg)} (ref {sum(ref_cg)}, "
+          f"ref det-vs-BLAS {ss.get('cg_total')}) du={du:.3e} dv={dv:.3e} "
+          f"(ref self-spread {ss.get('du', float('nan')):.2e}/{ss.get('dv', float('nan')):.2e})")
 
 
 @pytest.mark.parametrize("name", [n for n in traj_names() if not n.startswith("D")])

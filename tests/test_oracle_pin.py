@@ -36,7 +36,8 @@ def _trajectory(run):
 def test_oracle_matches_reference_bitwise(name):
     meta, arr = load_traj(name)
     prob = problems.workload(meta["spec"])
-    run = orc.mdot(prob.C, prob.r, prob.c, meta["gamma_i"], meta["gamma_f"])
+    run = orc.mdot(prob.C, prob.r, prob.c, meta["gamma_i"], meta["gamma_f"],
+                   projector=meta.get("projector", "newton"))
     assert np.array_equal(run.state.u, arr["u"])
     assert np.array_equal(run.state.v, arr["v"])
     assert run.primal == meta["primal"]
@@ -45,6 +46,31 @@ def test_oracle_matches_reference_bitwise(name):
     got = _trajectory(run)
     # json turns inf into Infinity -> float('inf'); compare as floats
     assert json_norm(got) == json_norm(ref)
+
+
+@pytest.mark.parametrize("name", traj_names())
+def test_every_golden_records_a_bitwise_oracle(name):
+    """make_golden.py --verify-oracle ran the oracle beside the reference on
+    every case, the n = 4096 D2 / D3 solves included (too slow for this
+    suite), and recorded whether it reproduced the reference bit for bit."""
+    meta, _ = load_traj(name)
+    assert meta.get("oracle_bitwise") is True
+
+
+def test_slab_threads_do_not_change_bits():
+    """The slab-parallel oracle (bench.py's CPU baseline) is bit-identical to
+    the serial one: every 256-row slab is an independent computation."""
+    prob = problems.workload("grid:32:l2sq:0")
+    runs = []
+    for k in (1, 4):
+        orc.set_threads(k)
+        try:
+            runs.append(orc.mdot(prob.C, prob.r, prob.c, 2.0 ** 5, 2.0 ** 10))
+        finally:
+            orc.set_threads(1)
+    assert np.array_equal(runs[0].state.u, runs[1].state.u)
+    assert np.array_equal(runs[0].P, runs[1].P)
+    assert runs[0].ops == runs[1].ops
 
 
 def json_norm(obj):

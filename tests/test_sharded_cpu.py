@@ -39,7 +39,8 @@ def _solve(comm):
     return dict(u=st._u.numpy().tolist(), v=st._v.numpy().tolist(),
                 cg=[it.stats.cg_iters for it in sol.iterations],
                 newton=[it.stats.newton_steps for it in sol.iterations],
-                primal=sol.primal_cost, ops=sol.report.ops, row0=cost.row0, row1=cost.row1)
+                primal=sol.primal_cost, ops=sol.report.ops, row0=cost.row0, row1=cost.row1,
+                stats=dict(comm.stats))
 
 
 def _worker(rank, world, port, out_path):
@@ -78,3 +79,11 @@ def test_two_rank_sharded_solve_matches_single_rank(tmp_path):
         np.testing.assert_allclose(s["v"], single["v"], rtol=1e-11, atol=1e-11)
         assert s["primal"] == pytest.approx(single["primal"], rel=1e-11)
     np.testing.assert_allclose(u, single["u"], rtol=1e-11, atol=1e-11)
+    # one allreduce per column-direction product (P^T x, and the column LSE
+    # against the previous LSE as shift), except the first column LSE of the
+    # solve (no shift yet: MAX + SUM) and any shift fallback (3 each); the
+    # streaming rounding adds its one column-sum allreduce (driver.py:196-198)
+    st = shards[0]["stats"]
+    fb = st.get("lse_shift_fallbacks", 0)
+    assert fb <= 1
+    assert st["vector_allreduces"] == st["column_products"] + 1 + 2 * fb + 1, st

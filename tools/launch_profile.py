@@ -24,7 +24,7 @@ def wrap(orig, sys_pos):
         TELEMETRY.time_coop = True
         n0 = len(TELEMETRY.coop)
         res = orig(*a)
-        ms, h, dv, n = TELEMETRY.coop[n0]
+        ms, h, dv, n, *_ = TELEMETRY.coop[n0]
         sys_ = a[sys_pos]
         k = sys_._ctx
         lay = np.zeros(k.coop_blocks + 2, dtype=np.int32)
