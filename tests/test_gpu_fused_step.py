@@ -171,8 +171,10 @@ def test_persistent_launch_timing():
     try:
         res, _, _ = _newton_step_device(st, st._system(), st._g, 0.5, 0.0, False, None, d, dv,
                                         ARMIJO_C1, ARMIJO_SLOPE_FLOOR)
-        ms, hvps, dvflag, n = TELEMETRY.coop[-1]
+        ms, hvps, dvflag, n, mode, nnz, span, cg = TELEMETRY.coop[-1]
         assert ms > 0.0 and hvps == res.hvps and n == st.n
+        assert mode == res.plan_mode and cg == res.cg_iters
+        assert 0 < nnz <= span <= n * st._ctx.ld
     finally:
         TELEMETRY.time_coop = False
     k = st._ctx
