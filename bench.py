@@ -57,7 +57,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "sec to ||r(P)-r||_1+||c(P)-c||_1<=1e-6 (n=4096)"
-METRIC_D4 = "sec to solve n=65536 on-the-fly 3-D OT (gamma 2^5->2^10), row-sharded"
+METRIC_D4 = "sec to solve n={n} on-the-fly 3-D OT (gamma 2^5->2^10), row-sharded"
 D2 = dict(spec="grid:64:l2sq:0", gamma_i=2.0 ** 5, gamma_f=2.0 ** 16, p=1.5, q_init=2.0)
 D2_GOLDEN = os.path.join(ROOT, "tests", "golden", "traj_D2_grid64_l2sq_s0.npz")
 D4_GAMMA = (2.0 ** 5, 2.0 ** 10)
@@ -484,7 +484,7 @@ def run_sharded(args, rank, world, dev):
         out_extras["d2_replicas"] = d2_replicas(dev, rank, world)
     val = statistics.mean(times)
     return {
-        "metric": METRIC_D4, "value": val, "unit": "s", "n_gpus": world,
+        "metric": METRIC_D4.format(n=n), "value": val, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": val * 1e3,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded U[0,1)^3 point clouds, uniform marginals)",
@@ -493,6 +493,8 @@ def run_sharded(args, rank, world, dev):
                 "d2h_bytes_per_step": 8},
         "gpu_launches": None,
         "solve": rec, "per_step_s": times, "clocks": clocks.summary(),
+        "collectives": {"backend": _BACKEND, "ranks": world,
+                        "per_solve": rec.get("collectives")},
         "extras": out_extras,
     }
 
@@ -599,6 +601,16 @@ def run_reference(args, world):
 _PG = None
 
 
+# BENCH_DIST_BACKEND=gloo + BENCH_DEVICE=0: every rank on cuda:0 with host-staged
+# allreduces -- only for the process-group test of this script on a one-GPU
+# box (tests/test_gpu_bench_sharded.py); a real run is one rank per GPU on NCCL.
+_BACKEND = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+
+
+def local_device():
+    return int(os.environ.get("BENCH_DEVICE", os.environ.get("LOCAL_RANK", 0)))
+
+
 def init_dist(args):
     global _PG
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -606,8 +618,8 @@ def init_dist(args):
     if world > 1 and args.impl != "reference":
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local_device())
+        dist.init_process_group(_BACKEND)
         _PG = dist
     return rank, world
 
@@ -620,7 +632,8 @@ def barrier(world):
 def max_over_ranks(x, world):
     if world > 1 and _PG is not None:
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64,
+                         device="cuda" if _BACKEND == "nccl" else "cpu")
         _PG.all_reduce(t, op=_PG.ReduceOp.MAX)
         return float(t.item())
     return x
@@ -666,7 +679,7 @@ def main():
             print(json.dumps(run_reference(args, world)))
         return
     import torch
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", local_device())
     torch.cuda.set_device(dev)
     if world == 1:
         out = run_d2(args, dev)
