@@ -387,12 +387,14 @@ def d4_solve(dev, n, comm=None):
     pc = ot.points_problem(n, 3, 0)
     cost = PointCloudCost(pc, dev, comm=comm)
     TELEMETRY.reset()
+    before = dict(comm.stats)
     torch.cuda.synchronize()
     comm.barrier()
     t0 = time.perf_counter()
     sol = ot.mdot(pc, D4_GAMMA[0], D4_GAMMA[1], cost=cost)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    collectives = {k: v - before.get(k, 0) for k, v in comm.stats.items()}
     passes = TELEMETRY.calls.get("otn_pc_pass", 0)
     st = sol.final_state
     st.set_targets(pc.r, pc.c)
@@ -403,7 +405,7 @@ def d4_solve(dev, n, comm=None):
            "sharding": f"rows over {comm.world} ranks" if comm.world > 1 else "none",
            "stages": len(sol.iterations), "cg": sum(i.stats.cg_iters for i in sol.iterations),
            "passes_per_rank": passes, "true_marginal_err": err, "primal": sol.primal_cost,
-           "collectives": dict(getattr(comm, "stats", {})),
+           "collectives": collectives,
            "entries_per_s_per_gpu": entries / dt,
            "fp64_pipe_frac_est": entries / dt / peak_entries,
            "fp64_basis": f"{PAIR_FP64_INSTR_PER_ENTRY} FP64 instr/entry (SASS), "

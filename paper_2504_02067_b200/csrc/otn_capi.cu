@@ -630,7 +630,7 @@ int otn_reduce_dev(otn_ctx* x, int64_t n, int op, const double* a, const double*
                    const double* c, const double* d, double* dev_out) {
   DeviceGuard dg_(x);
   OTN_REQUIRE(x && a && dev_out && n >= 0, "otn_reduce_dev: bad argument");
-  OTN_REQUIRE(op >= OTN_RED_SUM_EXP && op <= OTN_RED_OUTSIDE && op != OTN_RED_MAX,
+  OTN_REQUIRE(op >= OTN_RED_GRAD_L1 && op <= OTN_RED_OUTSIDE && op != OTN_RED_MAX,
               "otn_reduce_dev: bad op (sums only)");
   OTN_CUDA(otn::launch_reduce(x, op, n, a, b, c, d, dev_out, x->flags + 2), "otn_reduce_dev");
   return OTN_OK;
