@@ -138,6 +138,14 @@ int otn_coop_layout(otn_ctx* ctx, int* host);
  * vector bookkeeping (log-marginal caches, targets) on the ctx stream.     */
 int otn_copy(otn_ctx* ctx, double* dst, const double* src, int64_t n);
 int otn_upload(otn_ctx* ctx, double* dst, const double* host_src, int64_t n);
+/* Zero `bytes` bytes of device memory, stream-ordered (buffer setup without
+ * a framework fill kernel).                                                 */
+int otn_zero(otn_ctx* ctx, void* dst, int64_t bytes);
+/* Cost preparation, once per problem (dual.py:77-89): host_sym = (C == C^T)
+ * over the n x n block of the ld-strided C (synchronizes); otn_transpose
+ * writes C^T (padding columns 0) for the column passes of an asymmetric C.  */
+int otn_is_symmetric(otn_ctx* ctx, const double* C, int* host_sym);
+int otn_transpose(otn_ctx* ctx, double* out, const double* C);
 /* Synchronize and copy the four device status flags to the host:
  * [0] plan overflow, [1] nonpositive sums, [2] reduce domain, [3] rounding. */
 int otn_read_flags(otn_ctx* ctx, int* host4);
@@ -244,6 +252,11 @@ int otn_newton_step(otn_ctx* ctx, const double* P, const uint64_t* seg_mask, con
                     const double* log_c, double* trial, double* lc, double* lr, double* grad,
                     double armijo_c1, double slope_floor, otn_solve_result* host_res,
                     double* host_out, int* host_flags);
+/* host_out == NULL: otn_newton_step only enqueues (the host is free until
+ * the results are needed); otn_newton_step_wait synchronizes and fills
+ * host_res / host_out / host_flags as otn_newton_step would have.           */
+int otn_newton_step_wait(otn_ctx* ctx, otn_solve_result* host_res, double* host_out,
+                         int* host_flags);
 
 /* Telemetry: with timing on, every persistent-solver launch (the partition
  * kernel + k_coop) is bracketed by CUDA events; otn_coop_ms waits for the

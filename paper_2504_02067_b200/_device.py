@@ -58,9 +58,10 @@ LAUNCHES = {
     "otn_newton": 2, "otn_probe": 2,
     # newton (2) + gate + trial (1 | 2) + mass + gate + accept (u, v, lc) + row LSE
     # + row stats with the gradient
-    "otn_newton_step": 9,
+    "otn_newton_step": 9, "otn_newton_step_wait": 0,
     "otn_vec": 1, "otn_reduce": 1, "otn_row_stats": 1, "otn_accept": 1, "otn_reduce_async": 1, "otn_round_plan": 10, "otn_pc_pass": 1,
-    "otn_vec_n": 1, "otn_reduce_n": 1, "otn_reduce_dev": 1,
+    "otn_vec_n": 1, "otn_reduce_n": 1, "otn_reduce_dev": 1, "otn_zero": 0,
+    "otn_is_symmetric": 1, "otn_transpose": 1,
 }
 
 
@@ -161,10 +162,17 @@ class Context:
         return float(ms.value)
 
     # ---- buffers ---------------------------------------------------------
+    def zeros(self, shape, dtype=None):
+        """A zeroed device buffer: torch allocates (caching allocator), the
+        library zeroes it stream-ordered (a memset, no framework kernel)."""
+        t = torch()
+        buf = t.empty(shape, dtype=dtype or t.float64, device=self.device)
+        self.call("otn_zero", vptr(buf), buf.numel() * buf.element_size())
+        return buf
+
     def vec(self, init=None):
         """Padded device vector (ld entries, zeros beyond n); returns the buffer."""
-        t = torch()
-        buf = t.zeros(self.ld, dtype=t.float64, device=self.device)
+        buf = self.zeros(self.ld)
         if init is not None:
             self.upload(buf, init)
         return buf
@@ -227,13 +235,11 @@ class Context:
         return out
 
     def mat(self):
-        t = torch()
-        return t.zeros((self.n, self.ld), dtype=t.float64, device=self.device)
+        return self.zeros((self.n, self.ld))
 
     def seg_mask(self):
         """Plan segment-occupancy mask (OTN_MASK_WORDS(ld) uint64 words per row)."""
-        t = torch()
-        return t.zeros((self.n, (self.ld + 4095) // 4096 + 1), dtype=t.int64, device=self.device)
+        return self.zeros((self.n, (self.ld + 4095) // 4096 + 1), dtype=torch().int64)
 
     # ---- thin call helpers -----------------------------------------------
     def call(self, name, *args):
@@ -244,7 +250,25 @@ class Context:
 
 
 class DeviceCost:
-    """Device-resident cost matrix with leading dimension ld (multiple of 32)."""
+    """Device-resident cost matrix with leading dimension ld (multiple of 32).
+
+    For a problem whose C is already a CUDA tensor the prepared cost (the
+    symmetry verdict, an asymmetric cost's transpose) is kept on the Problem
+    and reused by later solves while the tensor is unchanged (same storage,
+    same torch version counter); a host C is uploaded by every solve."""
+
+    @classmethod
+    def of(cls, problem, device):
+        C = problem.C
+        if not (is_tensor(C) and C.is_cuda and C.device == device):
+            return cls(problem, device)
+        key = (C.data_ptr(), tuple(C.shape), tuple(C.stride()), C._version)
+        cached = problem.__dict__.get("_otn_device_cost")
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        dc = cls(problem, device)
+        problem.__dict__["_otn_device_cost"] = (key, dc)
+        return dc
 
     def __init__(self, problem, device):
         t = torch()
@@ -258,7 +282,7 @@ class DeviceCost:
             if ld == self.n and C.is_contiguous():
                 self.C = C
             else:
-                self.C = t.zeros((self.n, ld), dtype=t.float64, device=device)
+                self.C = self.ctx.zeros((self.n, ld))
                 self.C[:, : self.n].copy_(C)
         else:
             host = t.from_numpy(np.ascontiguousarray(C, dtype=np.float64))
@@ -266,16 +290,18 @@ class DeviceCost:
             if ld == self.n:
                 self.C = host.to(device, non_blocking=False)
             else:
-                self.C = t.zeros((self.n, ld), dtype=t.float64, device=device)
+                self.C = self.ctx.zeros((self.n, ld))
                 self.C[:, : self.n].copy_(host)
         self._symmetric = None
 
     @property
     def symmetric(self):
-        """(C == C.T).all(), evaluated once (dual.py:80-88)."""
+        """(C == C.T).all(), evaluated once (dual.py:80-88), by the library's
+        tiled comparison kernel."""
         if self._symmetric is None:
-            sq = self.C[:, : self.n]
-            self._symmetric = bool(torch().equal(sq, sq.t()))
+            flag = ctypes.c_int(0)
+            self.ctx.call("otn_is_symmetric", vptr(self.C), ctypes.byref(flag))
+            self._symmetric = bool(flag.value)
         return self._symmetric
 
     def ptr(self):
@@ -289,7 +315,6 @@ class DeviceCost:
         if self.symmetric:
             return vptr(self.C), 1
         if getattr(self, "CT", None) is None:
-            t = torch()
-            self.CT = t.zeros_like(self.C)
-            self.CT[:, : self.n].copy_(self.C[:, : self.n].t())
+            self.CT = self.ctx.zeros((self.n, self.ctx.ld))
+            self.ctx.call("otn_transpose", vptr(self.CT), vptr(self.C))
         return vptr(self.CT), 1

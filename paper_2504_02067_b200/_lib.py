@@ -101,6 +101,7 @@ SIGNATURES = {
                    ctypes.POINTER(SolveResult)],
     "otn_newton_step": [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I, _I64, _P, _P, _P, _P, _I, _D, _P, _P,
                         _P, _P, _P, _P, _P, _P, _D, _D, ctypes.POINTER(SolveResult), _DP, _IP],
+    "otn_newton_step_wait": [_P, ctypes.POINTER(SolveResult), _DP, _IP],
     "otn_probe": [_P, _P, _P, _P, _P, _P, _P, _I, _I64],
     "otn_coop_layout": [_P],
     "otn_pc_pass": [_P, _I, _P, _I64, _I64, _P, _I64, _I64, _I, _D, _D, _I, _P, _P, _D, _P, _P,
@@ -108,6 +109,9 @@ SIGNATURES = {
     "otn_vec_n": [_P, _I64, _I, _D, _P, _P, _P, _P, _P],
     "otn_reduce_n": [_P, _I64, _I, _P, _P, _P, _P, _DP, _IP],
     "otn_reduce_dev": [_P, _I64, _I, _P, _P, _P, _P, _P],
+    "otn_zero": [_P, _P, _I64],
+    "otn_is_symmetric": [_P, _P, _IP],
+    "otn_transpose": [_P, _P, _P],
     "otn_vec": [_P, _I, _D, _P, _P, _P, _P, _P],
     "otn_reduce": [_P, _I, _P, _P, _P, _P, _DP, _IP],
     "otn_row_stats": [_P, _P, _P, _P, _DP, _IP],

@@ -267,6 +267,31 @@ int otn_upload(otn_ctx* x, double* dst, const double* host_src, int64_t n) {
   return OTN_OK;
 }
 
+int otn_zero(otn_ctx* x, void* dst, int64_t bytes) {
+  DeviceGuard dg_(x);
+  OTN_REQUIRE(x && dst && bytes >= 0, "otn_zero: bad argument");
+  OTN_CUDA(cudaMemsetAsync(dst, 0, size_t(bytes), x->stream), "otn_zero");
+  return OTN_OK;
+}
+
+int otn_is_symmetric(otn_ctx* x, const double* C, int* host_sym) {
+  DeviceGuard dg_(x);
+  OTN_REQUIRE(x && C && host_sym, "otn_is_symmetric: NULL argument");
+  OTN_CUDA(cudaMemsetAsync(x->flags + 10, 0, sizeof(int), x->stream), "otn_is_symmetric: flag");
+  OTN_CUDA(otn::launch_symmetric(x, C, x->flags + 10), "otn_is_symmetric");
+  int rc = sync_copy(x, x->h_flags + 10, x->flags + 10, sizeof(int), "otn_is_symmetric: copy");
+  if (rc) return rc;
+  *host_sym = x->h_flags[10] == 0;
+  return OTN_OK;
+}
+
+int otn_transpose(otn_ctx* x, double* out, const double* C) {
+  DeviceGuard dg_(x);
+  OTN_REQUIRE(x && out && C && out != C, "otn_transpose: bad argument");
+  OTN_CUDA(otn::launch_transpose(x, out, C), "otn_transpose");
+  return OTN_OK;
+}
+
 int otn_coop_layout(otn_ctx* x, int* host) {
   DeviceGuard dg_(x);
   OTN_REQUIRE(x && host, "otn_coop_layout: NULL argument");
@@ -507,8 +532,7 @@ int otn_newton_step(otn_ctx* x, const double* P, const uint64_t* m, const double
                     int* host_flags) {
   DeviceGuard dg_(x);
   OTN_REQUIRE(x && P && rP && cP && mu && g && d_u && d_v && C && Ccols && u && v && r && log_c &&
-                  trial &&
-                  lc && lr && grad && host_out,
+                  trial && lc && lr && grad,
               "otn_newton_step: NULL argument");
   OTN_REQUIRE(max_iters >= 0, "otn_newton_step: max_iters < 0");
   otn::CoopArgs a = plan_args(x, P, m);
@@ -550,6 +574,14 @@ int otn_newton_step(otn_ctx* x, const double* P, const uint64_t* m, const double
                            cudaMemcpyDeviceToHost, x->stream), "otn_newton_step: copy");
   OTN_CUDA(cudaMemcpyAsync(x->h_flags + 6, x->flags + 6, 3 * sizeof(int), cudaMemcpyDeviceToHost,
                            x->stream), "otn_newton_step: copy");
+  if (!host_out) return OTN_OK;                     // collected by otn_newton_step_wait
+  return otn_newton_step_wait(x, host_res, host_out, host_flags);
+}
+
+int otn_newton_step_wait(otn_ctx* x, otn_solve_result* host_res, double* host_out,
+                         int* host_flags) {
+  DeviceGuard dg_(x);
+  OTN_REQUIRE(x && host_out, "otn_newton_step_wait: NULL argument");
   int rc = finish_solve(x, host_res, "otn_newton_step: result");
   const bool ran = x->h_flags[6] != 0, ok = x->h_flags[7] != 0;
   host_out[0] = ran ? x->h_scal[32] : 0.0;

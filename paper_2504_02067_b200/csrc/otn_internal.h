@@ -131,6 +131,8 @@ cudaError_t launch_accept(otn_ctx* x, double s, double* u, const double* du, dou
 constexpr int kRedRowStatsGrad = 100;
 cudaError_t launch_step_gate(otn_ctx* x, int stage, const DevResult* res, const double* mass,
                              double slope_floor, double armijo_c1, int* flags);
+cudaError_t launch_symmetric(otn_ctx* x, const double* C, int* flag);
+cudaError_t launch_transpose(otn_ctx* x, double* out, const double* C);
 cudaError_t launch_round(otn_ctx* x, double* P, const double* C, const double* r, const double* c,
                          double* scratch_scalars, int* flag);
 

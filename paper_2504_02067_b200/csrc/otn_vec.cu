@@ -343,4 +343,58 @@ cudaError_t launch_round(otn_ctx* x, double* P, const double* C, const double* r
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// cost-matrix preparation (once per problem): (C == C^T).all() and C^T,
+// 32 x 32 tiles through shared memory so both sides are read coalesced
+// (dual.py:80-88 forms K^T as a contiguous copy unless C is symmetric)
+// ---------------------------------------------------------------------------
+constexpr int kTp = 32;
+
+__global__ void __launch_bounds__(kTp * 8) k_symmetric(const double* C, int64_t n, int64_t ld,
+                                                       int* flag) {
+  __shared__ double tile[kTp][kTp + 1];
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  if (bj < bi) return;                               // upper-triangle tile pairs only
+  const int tx = threadIdx.x & (kTp - 1), ty = threadIdx.x / kTp;
+  // stage tile (bj, bi) transposed, compare with tile (bi, bj)
+  for (int y = ty; y < kTp; y += 8) {
+    const int64_t i = int64_t(bj) * kTp + y, j = int64_t(bi) * kTp + tx;
+    tile[tx][y] = (i < n && j < n) ? C[i * ld + j] : 0.0;
+  }
+  __syncthreads();
+  int bad = 0;
+  for (int y = ty; y < kTp; y += 8) {
+    const int64_t i = int64_t(bi) * kTp + y, j = int64_t(bj) * kTp + tx;
+    if (i < n && j < n && !(C[i * ld + j] == tile[y][tx])) bad = 1;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+__global__ void __launch_bounds__(kTp * 8) k_transpose(double* out, const double* C, int64_t n,
+                                                       int64_t ld) {
+  __shared__ double tile[kTp][kTp + 1];
+  const int tx = threadIdx.x & (kTp - 1), ty = threadIdx.x / kTp;
+  for (int y = ty; y < kTp; y += 8) {
+    const int64_t i = int64_t(blockIdx.y) * kTp + y, j = int64_t(blockIdx.x) * kTp + tx;
+    tile[y][tx] = (i < n && j < n) ? C[i * ld + j] : 0.0;
+  }
+  __syncthreads();
+  for (int y = ty; y < kTp; y += 8) {
+    const int64_t i = int64_t(blockIdx.x) * kTp + y, j = int64_t(blockIdx.y) * kTp + tx;
+    if (i < n && j < ld) out[i * ld + j] = tile[tx][y];   // padding columns get 0
+  }
+}
+
+cudaError_t launch_symmetric(otn_ctx* x, const double* C, int* flag) {
+  const unsigned t = unsigned((x->n + kTp - 1) / kTp);
+  k_symmetric<<<dim3(t, t), kTp * 8, 0, x->stream>>>(C, x->n, x->ld, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose(otn_ctx* x, double* out, const double* C) {
+  const unsigned tc = unsigned((x->ld + kTp - 1) / kTp);
+  k_transpose<<<dim3(tc, tc), kTp * 8, 0, x->stream>>>(out, C, x->n, x->ld);
+  return cudaGetLastError();
+}
+
 }  // namespace otn

@@ -26,12 +26,12 @@ from .errors import DomainError
 
 def device_cost(problem, device=None):
     """The problem's device-resident cost, created once per problem object."""
-    dc = getattr(problem, "_otn_device_cost", None)
+    dc = getattr(problem, "_otn_state_cost", None)
     dev = require_cuda(device)
     if dc is None or dc.ctx.device != dev:
-        dc = DeviceCost(problem, dev)
+        dc = DeviceCost.of(problem, dev)
         try:
-            problem._otn_device_cost = dc
+            problem._otn_state_cost = dc
         except AttributeError:
             pass
     else:
@@ -124,9 +124,10 @@ class DualState:
     def cache_valid(self):
         return self._cache_valid
 
-    def set_targets(self, r, c):
+    def set_targets(self, r, c, _logs=None):
         """Swap the target marginals (dual.py:64-67); logs are taken on the host
-        with numpy, exactly as the reference's np.log(r) / np.log(c).  The four
+        with numpy, exactly as the reference's np.log(r) / np.log(c) (mdot may
+        pass them precomputed: ``_logs`` = (np.log(r), np.log(c))).  The four
         device vectors are rewritten in place by stream-ordered copies from
         page-locked staging (no host stall); the same arrays again are a no-op."""
         r = np.asarray(r, dtype=np.float64)
@@ -139,13 +140,12 @@ class DualState:
         self.c = c
         k = self._ctx
         if getattr(self, "_tgt", None) is None:
-            t = torch()
             # r, c, log r, log c as rows of one device block: one H2D copy
-            self._tgt = t.zeros((4, k.ld), dtype=t.float64, device=k.device)
+            self._tgt = k.zeros((4, k.ld))
             self._r, self._c, self._log_r, self._log_c = self._tgt.unbind(0)
         with np.errstate(divide="ignore", invalid="ignore"):
-            k.upload_rows_async(self._tgt, (self.r, self.c, np.log(self.r), np.log(self.c)),
-                                "targets")
+            lr, lc = _logs if _logs is not None else (np.log(self.r), np.log(self.c))
+            k.upload_rows_async(self._tgt, (self.r, self.c, lr, lc), "targets")
         self._targets_copy = (self.r.copy(), self.c.copy())
         self._rowstat = None
 
@@ -341,8 +341,12 @@ class DualState:
         """Newton direction + first trial + (if accepted) accept path in one
         synchronization (otn_newton_step); see projector.project."""
         from .newton import _newton_step_device
+        # host work the driver queued for the next GPU-bound wait (mdot: the
+        # next stage's candidate targets), run while the GPU solves this step
+        prework = self.__dict__.pop("_prework", None)
         res, mass, rowstat = _newton_step_device(self, sys, self._g, eta, rho0, zero_init,
-                                                 max_cg_iters, d_u, d_v, armijo_c1, slope_floor)
+                                                 max_cg_iters, d_u, d_v, armijo_c1, slope_floor,
+                                                 prework=prework)
         if rowstat is not None:
             # the device ran _accept(1.0, d_u, d_v) + refresh_rows_only + _row_stats
             self._cache_valid = True

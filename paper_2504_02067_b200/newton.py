@@ -262,7 +262,7 @@ def _newton_device(grad_u, sys, eta, rho0, zero_init, max_cg_iters, d_u, d_v):
 
 
 def _newton_step_device(state, sys, grad_u, eta, rho0, zero_init, max_cg_iters, d_u, d_v,
-                        armijo_c1, slope_floor):
+                        armijo_c1, slope_floor, prework=None):
     """One otn_newton_step launch sequence for a DualState: the Newton
     direction, its trial at alpha = 1 and, when the Armijo test passes there,
     the accept path, with one host synchronization.  Returns
@@ -289,9 +289,17 @@ def _newton_step_device(state, sys, grad_u, eta, rho0, zero_init, max_cg_iters, 
                 vptr(state._trial_vec), vptr(state._lc), vptr(state._lr), vptr(state._g))
         cached = state._nstep_ptrs = (key, head, mid, tail)
     _, head, mid, tail = cached
-    k.call("otn_newton_step", *head, float(eta), float(rho0), int(bool(zero_init)),
-           int(max_cg_iters), *mid, state._ng, *tail,
-           float(armijo_c1), float(slope_floor), ctypes.byref(res), out, ctypes.byref(fl))
+    if prework is None:
+        k.call("otn_newton_step", *head, float(eta), float(rho0), int(bool(zero_init)),
+               int(max_cg_iters), *mid, state._ng, *tail,
+               float(armijo_c1), float(slope_floor), ctypes.byref(res), out, ctypes.byref(fl))
+    else:
+        # enqueue, do the caller's host work while the GPU runs the step, collect
+        k.call("otn_newton_step", *head, float(eta), float(rho0), int(bool(zero_init)),
+               int(max_cg_iters), *mid, state._ng, *tail,
+               float(armijo_c1), float(slope_floor), None, None, None)
+        prework()
+        k.call("otn_newton_step_wait", ctypes.byref(res), out, ctypes.byref(fl))
     if timed:
         TELEMETRY.coop.append((k.coop_ms(), int(res.hvps), 1, k.n, int(res.plan_mode),
                                int(res.plan_nnz), int(res.plan_span), int(res.cg_iters)))

@@ -339,7 +339,7 @@ class PointCloudState:
     def v(self):
         return self._v.cpu().numpy().copy()
 
-    def set_targets(self, r, c):
+    def set_targets(self, r, c, _logs=None):
         self.r = np.asarray(r, dtype=np.float64)
         self.c = np.asarray(c, dtype=np.float64)
         lo, hi = self._pc.row0, self._pc.row1

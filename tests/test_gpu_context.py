@@ -63,3 +63,23 @@ def test_device_solution_plan_is_not_overwritten():
     st.u = st.u + 0.01                       # a different plan
     DiscountedSystem.from_state(st)          # materializes into the state's buffer
     assert torch.equal(sol.P, keep)
+
+
+def test_device_solve_launches_only_library_kernels():
+    """A solve of a device-resident problem (after the first, which prepares
+    the cost) runs no framework kernels: every launch is the library's
+    (buffers are zeroed by memsets, the symmetry test and transpose are
+    library kernels, the prepared cost is reused)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    p = problems.workload("pix:1024:784:0")                     # asymmetric: transpose path
+    dp = problems.Problem(C=torch.from_numpy(p.C).cuda(), r=p.r, c=p.c)
+    mdot(dp, 2.0 ** 5, 2.0 ** 9)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        mdot(dp, 2.0 ** 5, 2.0 ** 9)
+        torch.cuda.synchronize()
+    kernels = {e.name for e in prof.events() if e.device_type.name == "CUDA"
+               and not e.name.lower().startswith(("memcpy", "memset"))}
+    foreign = sorted(k for k in kernels if "otn::" not in k)
+    assert kernels and not foreign, foreign
