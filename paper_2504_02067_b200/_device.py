@@ -119,6 +119,7 @@ class Context:
             _lib.check(rc, "otn_create")
         self.h = h
         self._stream = stream
+        self._fns = {}
         info = (ctypes.c_int64 * 4)()
         _lib.check(self.lib.otn_info(self.h, info), "otn_info")
         self.coop_blocks = int(info[2])
@@ -243,10 +244,20 @@ class Context:
 
     # ---- thin call helpers -----------------------------------------------
     def call(self, name, *args):
-        i = _SYM_ARG.get(name)
-        TELEMETRY.count(name, sym=bool(args[i]) if i is not None else False)
-        rc = getattr(self.lib, name)(self.h, *args)
-        return _lib.check(rc, name)
+        # the host issues ~450 calls per n = 4096 solve, many while the GPU
+        # waits on it: one cached lookup per call
+        ent = self._fns.get(name)
+        if ent is None:
+            ent = self._fns[name] = (getattr(self.lib, name), LAUNCHES.get(name, 0),
+                                     _SYM_ARG.get(name))
+        fn, k, si = ent
+        if si is not None and args[si]:
+            k -= 1                       # a symmetric cost: the column pass is one kernel
+        T = TELEMETRY
+        T.launches += k
+        T.calls[name] = T.calls.get(name, 0) + 1
+        rc = fn(self.h, *args)
+        return _lib.check(rc, name) if rc else rc
 
 
 class DeviceCost:

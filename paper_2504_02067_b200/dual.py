@@ -67,8 +67,16 @@ class DualState:
         self._ctx = self._dc.ctx
         k = self._ctx
         self._gamma = float(gamma)
-        self._u = k.vec(np.zeros(self.n) if u is None else u)
-        self._v = k.vec(np.zeros(self.n) if v is None else v)
+        # u and v as the two rows of one device block, filled by one
+        # stream-ordered copy from page-locked staging (no host stall)
+        self._uv = k.zeros((2, k.ld))
+        self._u, self._v = self._uv.unbind(0)
+        init = [np.zeros(self.n) if x is None else x for x in (u, v)]
+        if any(is_tensor(x) for x in init):
+            k.upload(self._u, init[0])
+            k.upload(self._v, init[1])
+        else:
+            k.upload_rows_async(self._uv, init, "uv")
         self._lr = k.vec()
         self._lc = k.vec()
         self._g = k.vec()
