@@ -128,6 +128,9 @@ int otn_destroy(otn_ctx* ctx);
 int otn_set_stream(otn_ctx* ctx, void* stream);
 /* out4 = {n, ld, persistent-solver CTAs, workspace bytes} */
 int otn_info(const otn_ctx* ctx, int64_t* out4);
+/* out4 = {SMs, row-LSE path (0 register streaming, >0 CTAs of the bulk-copy
+ * row LSE), column-reduction slabs, last configuration error code}          */
+int otn_config(const otn_ctx* ctx, int64_t* out4);
 /* Synchronize and copy the row partition and plan mode of the last
  * persistent-solver launch: host[0..G] = row boundaries of the G CTAs,
  * host[G+1] = plan mode (0 streamed ring, 2 sparse shared-memory rows, 3

@@ -124,6 +124,10 @@ class Context:
         _lib.check(self.lib.otn_info(self.h, info), "otn_info")
         self.coop_blocks = int(info[2])
         self.workspace_bytes = int(info[3])
+        cfg = (ctypes.c_int64 * 4)()
+        _lib.check(self.lib.otn_config(self.h, cfg), "otn_config")
+        self.config = {"sms": int(cfg[0]), "lse_bulk_ctas": int(cfg[1]),
+                       "lse_slabs": int(cfg[2]), "config_error": int(cfg[3])}
 
     @classmethod
     def get(cls, n, device):

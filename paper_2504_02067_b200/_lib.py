@@ -79,6 +79,7 @@ SIGNATURES = {
     "otn_destroy": [_P],
     "otn_set_stream": [_P, _P],
     "otn_info": [_P, ctypes.POINTER(_I64)],
+    "otn_config": [_P, ctypes.POINTER(_I64)],
     "otn_read_flags": [_P, _IP],
     "otn_set_timing": [_P, _I],
     "otn_coop_ms": [_P, ctypes.POINTER(ctypes.c_float)],

@@ -5,6 +5,7 @@
 
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -176,6 +177,13 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
   size_t o_wp = off; off += align_up(size_t(x->coop_blocks) * ld * sizeof(double), 256);
   size_t o_red = off; off += align_up(size_t(otn::kRedSlots) * otn::kRedStride * otn::kRedWidth * sizeof(double), 256);
   size_t o_lse = off; off += align_up(size_t(x->lse_slabs) * ld * 2 * sizeof(double), 256);
+  {
+    // the bulk-copy row LSE is opt-in (OTN_LSE_BULK=1): measured slower than
+    // the register-streaming kernel on B200 (tools/lse_bench.py)
+    const char* bulk = std::getenv("OTN_LSE_BULK");
+    x->lse_bulk_ctas = (bulk && bulk[0] == '1') ? otn::lse_bulk_grid(x->num_sms, n, ld, &x->cfg_err)
+                                                : 0;
+  }
   size_t o_sc = off; off += align_up(64 * sizeof(double), 256);
   size_t o_fl = off; off += align_up(16 * sizeof(int), 256);
   size_t o_res = off; off += align_up(sizeof(otn::DevResult), 256);
@@ -206,6 +214,7 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
   x->wpart = (double*)(base + o_wp);
   x->red = (double*)(base + o_red);
   x->lse_part = (double*)(base + o_lse);
+
   x->scal = (double*)(base + o_sc);
   x->flags = (int*)(base + o_fl);
   x->dres = (otn::DevResult*)(base + o_res);
@@ -248,6 +257,15 @@ int otn_info(const otn_ctx* x, int64_t* out4) {
   out4[1] = x->ld;
   out4[2] = x->coop_blocks;
   out4[3] = int64_t(x->ws_bytes);
+  return OTN_OK;
+}
+
+int otn_config(const otn_ctx* x, int64_t* out4) {
+  OTN_REQUIRE(x && out4, "otn_config: NULL argument");
+  out4[0] = x->num_sms;
+  out4[1] = x->lse_bulk_ctas;
+  out4[2] = x->lse_slabs;
+  out4[3] = x->cfg_err;
   return OTN_OK;
 }
 

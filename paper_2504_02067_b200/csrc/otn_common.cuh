@@ -142,6 +142,29 @@ __device__ __forceinline__ double exp_tab_nc(double x, const double2* __restrict
   return (y * pow2i(e1)) * pow2i(e - e1);
 }
 
+// exp(x) for -707 <= x <= 0, the log-sum-exp terms against the row maximum:
+// exp_tab_nc's reduction and polynomial, but the result is normal, so 2^e is
+// applied by adding e to the exponent field (one integer add instead of two
+// power-of-two multiplies; identical bits).  Terms below -707 are < 1e-307
+// next to the maximum's own exp(0) = 1 and are skipped by the callers (the
+// per-lane sums they would enter are >= 1 or are merged into one that is:
+// adding them changes no bit).
+__device__ __forceinline__ double exp_m707(double x, const double2* __restrict__ tab) {
+  const double t = fma(x, kExpTabC[0], 6755399441055744.0);   // 64/ln2, 1.5*2^52 shifter
+  const int k = __double2loint(t);
+  const double kd = t - 6755399441055744.0;
+  double r = fma(-kd, kExpTabC[1], x);
+  r = fma(-kd, kExpTabC[2], r);
+  double q = fma(r, kExpTabC[3], kExpTabC[4]);
+  q = fma(q, r, kExpTabC[5]);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = q * r;
+  const double2 tj = tab[k & 63];
+  const double y = tj.x + fma(tj.x, q, tj.y);
+  return __hiloint2double(__double2hiint(y) + ((k >> 6) << 20), __double2loint(y));
+}
+
 __device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ tab) {
   return exp_tab_nc(x < -746.0 ? -746.0 : (x > 710.0 ? 710.0 : x), tab);
 }

@@ -50,6 +50,8 @@ struct otn_ctx {
   double* wpart;          // coop_blocks x ld column partials
   double* red;            // kRedSlots x coop_blocks x kRedWidth grid-reduction partials
   double* lse_part;       // lse_slabs x ld x 2 (m, s) column-LSE partials
+  int lse_bulk_ctas;      // persistent CTAs of the bulk-copy row LSE (0: register streaming)
+  int cfg_err;            // first error while configuring optional kernels (diagnostic)
   double* scal;           // 64 device scalars
   int* flags;             // 16 device flag words
   int* part;              // coop_blocks + 2 ints: row partition + plan mode (k_partition)
@@ -67,6 +69,7 @@ struct otn_ctx {
 namespace otn {
 // gate (nullable): a device flag; the launch does nothing when *gate == 0
 // (otn_newton_step enqueues the accept path before the host sees the result).
+int lse_bulk_grid(int num_sms, int64_t n, int64_t ld, int* err);
 cudaError_t launch_lse_rows(otn_ctx* x, const double* C, double ng, const double* outer,
                             const double* outer_d, const double* inner, const double* inner_d,
                             double alpha, int mode, double* out, const int* gate = nullptr);

@@ -122,6 +122,193 @@ __global__ void __launch_bounds__(kLseRowThreads) k_lse_rows(LseArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Row LSE through the bulk-copy (TMA) engine, persistent (ld <= 4096).
+//
+// A 1-D cp.async.bulk request is served by the SM's copy engine one request
+// after another (measured, tools/l2stream.cu: 4 KB requests stream at ~12
+// GB/s per SM whatever the ring depth; whole 32 KB rows reach the SM's HBM
+// share, tools/bulk_rows.cu: 6.7 TB/s chip-wide), so each request here is a
+// WHOLE row of C (up to 32 KB, contiguous).  CTA b (one per SM) owns rows
+// [b n / G, (b+1) n / G).  It stages the inner vector once (with its alpha *
+// direction term for the trial sums, formed once); a producer lane streams
+// the rows into a kRowStages-deep ring (full / empty mbarriers).  kRowGroups
+// groups of 8 warps take the rows in turn (group g: rows g, g + kRowGroups,
+// ...), warp w of a group holding 512 columns: the group first takes the row max
+// (warp maxima through shared memory, a named barrier), then sums
+// exp(b - max) over its entries (entries below -746 add an exact 0 and are
+// skipped, as everywhere), and the group's first warp adds the 8 partial sums
+// in warp order -- deterministic; numpy's own max-then-sum form
+// (_kernels.py:33-40).
+// ---------------------------------------------------------------------------
+constexpr int kRowW = 4096;                         // columns staged per row (ld <= kRowW)
+constexpr int kRowGroup = 8;                        // warps per row: 512 columns each
+constexpr int kRowGroups = 3;                       // rows being reduced at once
+constexpr int kRowStages = 6;                       // rows in flight (ring depth)
+constexpr int kRowThreads = (kRowGroups * kRowGroup + 1) * 32;   // + the producer warp
+constexpr size_t kRowSmem = size_t(kRowStages + 1) * kRowW * 8;  // ring + inner vector
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
+                                          uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}\n"
+      ::"r"(bar), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void group_sync(int id) {   // the 8 warps of one stage
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kRowGroup * 32) : "memory");
+}
+
+template <bool DIR>
+__global__ void __launch_bounds__(kRowThreads) k_lse_rows_bulk(LseArgs a) {
+  extern __shared__ __align__(128) double s_dyn[];  // [kRowStages][kRowW] rows, [kRowW] inner
+  __shared__ double2 s_exp[64];
+  __shared__ __align__(8) uint64_t s_full[kRowStages], s_empty[kRowStages], s_inbar;
+  __shared__ double s_pm[kRowGroups][kRowGroup], s_ps[kRowGroups][kRowGroup];
+  if (a.gate && *a.gate == 0) return;               // uniform over the grid
+  double* s_in = s_dyn + size_t(kRowStages) * kRowW;
+  const int G = gridDim.x;
+  const int64_t r0 = (int64_t(blockIdx.x) * a.n) / G, r1 = (int64_t(blockIdx.x + 1) * a.n) / G;
+  const int rows = int(r1 - r0);
+  const uint32_t bytes = uint32_t(a.ld) * 8u;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRowStages; ++s) {
+      mbar_init(smem_addr(&s_full[s]), 1);
+      mbar_init(smem_addr(&s_empty[s]), kRowGroup);
+    }
+    mbar_init(smem_addr(&s_inbar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the inner vector (and its direction, parked in stage 0 until combined)
+    mbar_expect_tx(smem_addr(&s_inbar), bytes * (DIR ? 2u : 1u));
+    bulk_load(smem_addr(s_in), a.inner, bytes, smem_addr(&s_inbar));
+    if (DIR) bulk_load(smem_addr(s_dyn), a.inner_d, bytes, smem_addr(&s_inbar));
+  }
+  exp_tab_load(s_exp);
+  __syncthreads();                                  // barriers initialized, table loaded
+  mbar_wait(smem_addr(&s_inbar), 0);
+  if (DIR) {                                        // numpy: base + alpha*dir (dual.py:174-175)
+    for (int j = threadIdx.x; j < int(a.ld); j += kRowThreads)
+      s_in[j] = __dadd_rn(s_in[j], __dmul_rn(a.alpha, s_dyn[j]));
+    __syncthreads();                                // stage 0 free again
+  }
+  if (warp == kRowGroups * kRowGroup) {             // producer
+    if (lane == 0) {
+      for (int it = 0; it < rows; ++it) {
+        const int s = it % kRowStages;
+        if (it >= kRowStages) mbar_wait(smem_addr(&s_empty[s]), uint32_t(it / kRowStages - 1) & 1u);
+        const uint32_t full = smem_addr(&s_full[s]);
+        mbar_expect_tx(full, bytes);
+        bulk_load(smem_addr(s_dyn + size_t(s) * kRowW), a.C + (r0 + it) * a.ld, bytes, full);
+      }
+    }
+    return;
+  }
+  const int g = warp / kRowGroup, gw = warp % kRowGroup;   // group, warp within the group
+  const int cb = gw * (kRowW / kRowGroup);                  // this warp's 512 columns
+  for (int it = g; it < rows; it += kRowGroups) {
+    const int s = it % kRowStages;
+    const double* crow = s_dyn + size_t(s) * kRowW;
+    mbar_wait(smem_addr(&s_full[s]), uint32_t(it / kRowStages) & 1u);
+    double b[16];
+    double wm = OTN_NINF;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = cb + 256 * h + 64 * k + 2 * lane;
+        double2 c = make_double2(0.0, 0.0), in = make_double2(0.0, 0.0);
+        if (j < int(a.ld)) {
+          c = *reinterpret_cast<const double2*>(&crow[j]);
+          in = *reinterpret_cast<const double2*>(&s_in[j]);
+        }
+        b[8 * h + 2 * k] = j < a.n ? __dadd_rn(__dmul_rn(a.ng, c.x), in.x) : OTN_NINF;
+        b[8 * h + 2 * k + 1] = j + 1 < a.n ? __dadd_rn(__dmul_rn(a.ng, c.y), in.y) : OTN_NINF;
+        wm = fmax(wm, fmax(b[8 * h + 2 * k], b[8 * h + 2 * k + 1]));
+      }
+    }
+    wm = warp_max(wm);
+    if (lane == 0) s_pm[g][gw] = wm;
+    group_sync(1 + g);
+    double M = s_pm[g][0];
+#pragma unroll
+    for (int w = 1; w < kRowGroup; ++w) M = fmax(M, s_pm[g][w]);
+    double sum = 0.0;
+    if (M != OTN_NINF) {
+      // entries more than 707 below the row max add nothing (exp_m707); a
+      // warp with no live entry in its 512 columns skips them all (late
+      // stages: most warps), the others run the 16 exps straight-line
+      bool any = false;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        b[k] = b[k] - M;
+        any |= b[k] >= -707.0;
+      }
+      if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const bool live = b[k] >= -707.0;
+          const double e = exp_m707(live ? b[k] : 0.0, s_exp);
+          sum = live ? sum + e : sum;
+        }
+      }
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) s_ps[g][gw] = sum;
+    group_sync(1 + g);
+    if (gw == 0 && lane == 0) {
+      double ss = s_ps[g][0];
+#pragma unroll
+      for (int w = 1; w < kRowGroup; ++w) ss += s_ps[g][w];
+      const int64_t row = r0 + it;
+      a.out[row] = finish(a, row, lse_value(M, ss));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_addr(&s_empty[s]));    // row data released
+    // (the next row's maxima overwrite s_pm only after this group's second
+    // barrier, so s_ps / s_pm of this row are never read stale)
+  }
+}
+
+// Persistent grid of the bulk-copy row LSE (one CTA per SM when it fits);
+// 0 when the row is too wide or the kernel cannot be configured.
+int lse_bulk_grid(int num_sms, int64_t n, int64_t ld, int* err) {
+  if (ld > kRowW) return 0;
+  cudaError_t e = cudaFuncSetAttribute(k_lse_rows_bulk<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRowSmem));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_lse_rows_bulk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kRowSmem));
+  int per = 0;
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_lse_rows_bulk<true>, kRowThreads,
+                                                      kRowSmem);
+  if (e != cudaSuccess || per < 1) {
+    *err = e != cudaSuccess ? int(e) : -1;
+    cudaGetLastError();
+    return 0;
+  }
+  const int64_t g = int64_t(per) * num_sms;
+  return int(g < n ? g : n);
+}
+
+// ---------------------------------------------------------------------------
 // Column LSE (asymmetric C): CTA = 64 columns x one slab of rows; each warp
 // walks rows 4 at a time (coalesced 512-byte row segments), lanes own 2
 // columns.  Partial (max, sum) per slab go to the workspace and a finalize
@@ -375,6 +562,13 @@ cudaError_t launch_lse_rows(otn_ctx* x, const double* C, double ng, const double
                             const double* outer_d, const double* inner, const double* inner_d,
                             double alpha, int mode, double* out, const int* gate) {
   LseArgs a{C, x->n, x->ld, ng, outer, outer_d, inner, inner_d, alpha, mode, out, gate};
+  if (x->lse_bulk_ctas > 0) {                       // whole rows through the copy engine
+    if (inner_d)
+      k_lse_rows_bulk<true><<<x->lse_bulk_ctas, kRowThreads, kRowSmem, x->stream>>>(a);
+    else
+      k_lse_rows_bulk<false><<<x->lse_bulk_ctas, kRowThreads, kRowSmem, x->stream>>>(a);
+    return cudaGetLastError();
+  }
   // full tiles (n a multiple of the 256-column step and of the rows per block):
   // no bounds predicates in the streaming loop
   if (x->n % 256 == 0)

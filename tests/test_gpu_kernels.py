@@ -308,3 +308,36 @@ class TestLambda2:
         P = np.full((n, n), 1.0 / (n * n))
         with pytest.raises(RefusalError):
             lambda2(DiscountedSystem(P, P.sum(axis=1), P.sum(axis=0)))
+
+
+def test_bulk_copy_row_lse_matches_oracle():
+    """The opt-in bulk-copy (TMA) row LSE (OTN_LSE_BULK=1, read when a context
+    is created: a fresh process) against the oracle, plain and with the
+    trial direction, at a full and a ragged size."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+from test_gpu_kernels import make_state, oracle_state
+from oracle import otn_oracle as orc
+from paper_2504_02067_b200 import DualState
+for n, sym in ((4096, True), (1000, False), (33, True)):
+    prob, u, v = make_state(n, seed=n, symmetric=sym)
+    st = DualState(prob, 4.0, u=u, v=v)
+    assert st._ctx.config["lse_bulk_ctas"] > 0, st._ctx.config
+    ref = oracle_state(prob, 4.0, u, v)
+    np.testing.assert_allclose(st.log_rP, ref.log_r, rtol=1e-13)
+    du = np.random.default_rng(1).standard_normal(n) * 0.1
+    dv = np.random.default_rng(2).standard_normal(n) * 0.1
+    got = st.trial_log_col_sums(du, dv, 0.5)
+    want = ref.trial_log_c(du, dv, 0.5)
+    np.testing.assert_allclose(got, want, rtol=1e-13)
+print("bulk ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env=dict(os.environ, OTN_LSE_BULK="1"), timeout=600)
+    assert out.returncode == 0 and "bulk ok" in out.stdout, out.stderr[-3000:]
