@@ -31,7 +31,7 @@ cost); the metric is seconds per solve (lower is better).
 N > 1 (``--gpus N`` re-executes itself under torch.distributed.run when not
 already launched that way): the headline is the ROW-SHARDED on-the-fly solve
 D4 (BASELINE configs[3]): n = 65536 3-D points, L2^2 cost recomputed in every
-pass, gamma 2^5 -> 2^10, rank g owning rows [g n/N, (g+1) n/N) with one NCCL
+pass, gamma 2^5 -> 2^10 (``--sharded d5``: D5, n = 2^20, BASELINE configs[4]), rank g owning rows [g n/N, (g+1) n/N) with one NCCL
 allreduce per column-direction product; strong scaling (same n at every N);
 value = max over ranks of the solve time.  ``extras.d4_1gpu`` is the same solve
 on rank 0's GPU alone (the scaling reference), ``extras.d2_replicas`` the D2
@@ -456,10 +456,11 @@ def run_sharded(args, rank, world, dev):
     from paper_2504_02067_b200._device import TELEMETRY
     from paper_2504_02067_b200.pointcloud import Comm, PointCloudCost
     comm = Comm()
-    n = args.d4_n or 65536
+    n = 2 ** 20 if args.sharded == "d5" else (args.d4_n or 65536)
     out_extras = {}
-    # the 1-GPU reference solve of the same n on rank 0 (strong-scaling basis)
-    if rank == 0 and not args.no_extras:
+    # the 1-GPU reference solve of the same n on rank 0 (strong-scaling basis;
+    # D5 on one GPU takes ~10 min: profiles/r01_d5_solve.json instead)
+    if rank == 0 and not args.no_extras and n <= 2 ** 17:
         dt1, rec1 = d4_solve(dev, n, comm=Comm.local())
         rec1["s"] = dt1
         out_extras["d4_1gpu"] = rec1
@@ -671,6 +672,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--d4-n", type=int, default=65536)
+    ap.add_argument("--sharded", choices=["d4", "d5"], default="d4",
+                    help="N > 1 workload: D4 (n = 65536, --d4-n) or D5 (n = 2^20)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
