@@ -72,7 +72,8 @@ CONFIG_D2 = {
 
 
 def config_d4(n, world):
-    return {"workload": f"D4 n={n} 3-D uniform points on-the-fly L2^2 gamma 2^5->2^10",
+    tag = "D5" if n >= 2 ** 20 else "D4"
+    return {"workload": f"{tag} n={n} 3-D uniform points on-the-fly L2^2 gamma 2^5->2^10",
             "n": n, "gamma_i": D4_GAMMA[0], "gamma_f": D4_GAMMA[1],
             "parallelism": f"rows{world}",
             "l2": "no n x n array exists: every pass recomputes the cost from the points"}
