@@ -102,3 +102,18 @@ def test_point_cloud_cost_matches_stored_cost():
     pc = problems.points_problem(64, 3, 0)
     dense = problems.dense_points_problem(64, 3, 0)
     np.testing.assert_array_equal(pc.materialize_cost(), dense.C)
+
+
+def test_seam_binding_declares_header_symbols():
+    """integration/otnewton_b200.py (the executable INTEGRATION.md §2 binding)
+    declares only entry points of include/otn_b200.h, with the same argument
+    counts as the package's own binding."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "otnewton_b200", os.path.join(ROOT, "integration", "otnewton_b200.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    declared = set(declared_symbols())
+    for name, (args, _) in mod._SIGS.items():
+        assert name in declared, name
+        assert len(args) == len(_lib.SIGNATURES[name]), name

@@ -20,10 +20,10 @@ rows = []
 
 
 def wrap(orig, sys_pos):
-    def wrapped(*a):
+    def wrapped(*a, **kw):
         TELEMETRY.time_coop = True
         n0 = len(TELEMETRY.coop)
-        res = orig(*a)
+        res = orig(*a, **kw)
         ms, h, dv, n, *_ = TELEMETRY.coop[n0]
         sys_ = a[sys_pos]
         k = sys_._ctx
