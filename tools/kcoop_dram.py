@@ -33,22 +33,22 @@ for k, lid in enumerate(ids):
     dram = m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
     mode, _, nnz, hvps, _us = lp[k][:5]
     launches.append({"mode": int(mode), "hvps": int(hvps), "dram_bytes": dram,
-                     "alg_bytes": 2 * nn8 * int(hvps) + nn8,
+                     "dense_bytes": 2 * nn8 * int(hvps) + nn8,
                      "ncu_us": m.get("gpu__time_duration.sum", 0) * 1e6})
 tot_dram = sum(l["dram_bytes"] for l in launches)
-tot_alg = sum(l["alg_bytes"] for l in launches)
+tot_alg = sum(l["dense_bytes"] for l in launches)
 by_mode = {}
 for l in launches:
-    b = by_mode.setdefault(str(l["mode"]), {"launches": 0, "hvps": 0, "dram_bytes": 0.0, "alg_bytes": 0.0})
+    b = by_mode.setdefault(str(l["mode"]), {"launches": 0, "hvps": 0, "dram_bytes": 0.0, "dense_bytes": 0.0})
     b["launches"] += 1
     b["hvps"] += l["hvps"]
     b["dram_bytes"] += l["dram_bytes"]
-    b["alg_bytes"] += l["alg_bytes"]
+    b["dense_bytes"] += l["dense_bytes"]
 res = {"source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
                  "-k regex:k_coop, one D2 L2^2 n=4096 solve (tools/profile_step.py)",
        "launches": len(launches), "dram_bytes_per_launch": tot_dram / max(len(launches), 1),
-       "alg_bytes_per_launch": tot_alg / max(len(launches), 1),
-       "traffic_bytes_per_alg_byte": tot_dram / tot_alg, "by_plan_mode": by_mode}
+       "dense_bytes_per_launch": tot_alg / max(len(launches), 1),
+       "traffic_bytes_per_dense_byte": tot_dram / tot_alg, "by_plan_mode": by_mode}
 json.dump(res, open("profiles/kcoop_traffic.json", "w"), indent=1)
 print(json.dumps({k: v for k, v in res.items() if k != "by_plan_mode"}, indent=1))
 print(json.dumps(by_mode, indent=1))
