@@ -335,7 +335,10 @@ def run_d2(args, dev):
 # ---------------------------------------------------------------------------
 # extras (N = 1): the other configurations, one timed solve each
 # ---------------------------------------------------------------------------
-PAIR_FP64_INSTR_PER_ENTRY = 32     # ncu: 31.1 (product pass) / 33.2 (log-sum-exp pass) at d = 3
+# FP64-pipe instructions per plan entry of the on-the-fly passes at d = 3 (ncu
+# smsp__inst_executed_pipe_fp64 x 32 / entries, n = 65536, separable exponent:
+# 21.2 for the product pass; 32 with the exact-cost exponent, OTN_PC_EXACT=1)
+PAIR_FP64_INSTR_PER_ENTRY = 21
 
 
 def fused_px(dev, peak, reps=200):

@@ -180,6 +180,8 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
   {
     // the bulk-copy row LSE is opt-in (OTN_LSE_BULK=1): measured slower than
     // the register-streaming kernel on B200 (tools/lse_bench.py)
+    const char* exact = std::getenv("OTN_PC_EXACT");  // separable exponent off (A/B)
+    x->pc_exact = exact && exact[0] == '1';
     const char* bulk = std::getenv("OTN_LSE_BULK");
     x->lse_bulk_ctas = (bulk && bulk[0] == '1') ? otn::lse_bulk_grid(x->num_sms, n, ld, &x->cfg_err)
                                                 : 0;

@@ -52,6 +52,7 @@ struct otn_ctx {
   double* lse_part;       // lse_slabs x ld x 2 (m, s) column-LSE partials
   int lse_bulk_ctas;      // persistent CTAs of the bulk-copy row LSE (0: register streaming)
   int cfg_err;            // first error while configuring optional kernels (diagnostic)
+  int pc_exact;           // on-the-fly passes: exact-cost exponent everywhere (OTN_PC_EXACT=1)
   double* scal;           // 64 device scalars
   int* flags;             // 16 device flag words
   int* part;              // coop_blocks + 2 ints: row partition + plan mode (k_partition)

@@ -50,7 +50,27 @@ __device__ __forceinline__ double pc_cost(const double* a, const double* b, doub
   return cmax > 0.0 ? div_cmax(s, cmax, rc) : s;
 }
 
-template <int RW, int D, int OP, int MB = 2>
+template <int D>
+__device__ __forceinline__ double sep_exponent(const double* x, const double* y, double Ai,
+                                               double Bj, double G) {
+  double d = x[0] * y[0];
+#pragma unroll
+  for (int k = 1; k < D; ++k) d = fma(x[k], y[k], d);
+  return fma(G, d, Ai + Bj);
+}
+
+// Plan exponent in separable form (SEP, the exp passes only): with
+//   C_ij = (|x_i|^2 + |y_j|^2 - 2 x_i.y_j) / C_max,
+//   e_ij = ng C_ij + v_j + u_i = (A_i + B_j) + G (x_i . y_j),
+// A_i = (ng/C_max)|x_i|^2 + u_i per row (registers), B_j = (ng/C_max)|y_j|^2
+// + v_j per column (staged with the tile), G = -2 ng/C_max: D FMAs, one add
+// and one FMA per entry instead of the exact-cost path's ~14 FP64 operations
+// (the exact path rounds C_ij itself to match a host-materialized cost
+// bit for bit; the separable one differs from it by a few units in the last
+// place of the exponent, ~1e-13 relative in a plan entry: inside every
+// parity gate, tests/test_gpu_pointcloud.py).  OTN_PC_EXACT=1 selects the
+// exact path for every pass.
+template <int RW, int D, int OP, int MB = 2, bool SEP = false>
 __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
   __shared__ double sb[D][kPcTile];
   __shared__ double scp[kPcTile];
@@ -60,6 +80,8 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
   const double rc = p.cmax > 0.0 ? __drcp_rn(p.cmax) : 0.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t i0 = (int64_t(blockIdx.x) * 8 + warp) * RW;
+  const double ngc = __dmul_rn(p.ng, rc);            // SEP: ng / C_max
+  const double G = -2.0 * ngc;
   double a[RW][D], rp[RW];
   double m[RW], s[RW];
 #pragma unroll
@@ -68,6 +90,12 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
 #pragma unroll
     for (int k = 0; k < D; ++k) a[r][k] = i < p.na ? __ldg(p.A + k * p.lda + i) : 0.0;
     rp[r] = (p.rowpot && i < p.na) ? __ldg(p.rowpot + i) : 0.0;
+    if (SEP) {                                       // rp becomes A_i
+      double nx = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) nx = fma(a[r][k], a[r][k], nx);
+      rp[r] = fma(ngc, nx, rp[r]);
+    }
     m[r] = (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART || OP == OTN_PC_MAXD || OP == OTN_PC_DIAG)
                ? OTN_NINF : 0.0;
     if (OP == OTN_PC_LSE_SHIFT) m[r] = i < p.na ? __ldg(p.outer + i) : 0.0;   // fixed shift
@@ -85,6 +113,12 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
         cp = __ldg(p.colpot + j);
         if (p.colpot_d) cp = __dadd_rn(cp, __dmul_rn(p.alpha, __ldg(p.colpot_d + j)));
       }
+      if (SEP) {                                     // scp becomes B_j
+        double ny = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) ny = fma(sb[k][t], sb[k][t], ny);
+        cp = fma(ngc, ny, cp);
+      }
       scp[t] = cp;
       svec[t] = (ok && p.vec) ? __ldg(p.vec + j) : 0.0;
     }
@@ -101,9 +135,14 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
             double bb[D];
 #pragma unroll
             for (int k = 0; k < D; ++k) bb[k] = sb[k][t];
-            const double c = pc_cost<D>(a[r], bb, p.cmax, rc);
-            double e = __dadd_rn(__dmul_rn(p.ng, c), scp[t]);
-            if (p.rowpot) e = __dadd_rn(e, rp[r]);
+            double e;
+            if (SEP) {
+              e = sep_exponent<D>(a[r], bb, rp[r], scp[t], G);
+            } else {
+              const double c = pc_cost<D>(a[r], bb, p.cmax, rc);
+              e = __dadd_rn(__dmul_rn(p.ng, c), scp[t]);
+              if (p.rowpot) e = __dadd_rn(e, rp[r]);
+            }
             s[r] += exp_tab(__dsub_rn(e, m[r]), s_exp);
           }
         }
@@ -121,9 +160,13 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
             double bb[D];
 #pragma unroll
             for (int k = 0; k < D; ++k) bb[k] = sb[k][t];
-            const double c = pc_cost<D>(a[r], bb, p.cmax, rc);
-            e[q] = __dadd_rn(__dmul_rn(p.ng, c), scp[t]);
-            if (p.rowpot) e[q] = __dadd_rn(e[q], rp[r]);
+            if (SEP) {
+              e[q] = sep_exponent<D>(a[r], bb, rp[r], scp[t], G);
+            } else {
+              const double c = pc_cost<D>(a[r], bb, p.cmax, rc);
+              e[q] = __dadd_rn(__dmul_rn(p.ng, c), scp[t]);
+              if (p.rowpot) e[q] = __dadd_rn(e[q], rp[r]);
+            }
           } else {
             e[q] = OTN_NINF;
           }
@@ -146,15 +189,20 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
         const double cpj = scp[t], vj = svec[t];
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
-          const double c = pc_cost<D>(a[r], bb, p.cmax, rc);
+          const double c = SEP ? 0.0 : pc_cost<D>(a[r], bb, p.cmax, rc);
           if (OP == OTN_PC_MAXD) {
             m[r] = fmax(m[r], c);
           } else if (OP == OTN_PC_CDOT) {
             s[r] = fma(c, vj, s[r]);
           } else {
-            const double kc = __dmul_rn(p.ng, c);
-            const double e = p.order == 0 ? __dadd_rn(__dadd_rn(kc, cpj), rp[r])
-                                          : __dadd_rn(__dadd_rn(kc, rp[r]), cpj);
+            double e;
+            if (SEP) {
+              e = sep_exponent<D>(a[r], bb, rp[r], cpj, G);
+            } else {
+              const double kc = __dmul_rn(p.ng, c);
+              e = p.order == 0 ? __dadd_rn(__dadd_rn(kc, cpj), rp[r])
+                               : __dadd_rn(__dadd_rn(kc, rp[r]), cpj);
+            }
             const double pe = exp_tab(e, s_exp);
             if (OP == OTN_PC_DOT) {
               s[r] = fma(pe, vj, s[r]);
@@ -205,9 +253,14 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
 }
 
 template <int RW, int D, int OP, int MB = 2>
-static cudaError_t launch_rw(const PairArgs& p, cudaStream_t st) {
+static cudaError_t launch_rw(const PairArgs& p, cudaStream_t st, bool sep) {
   const int64_t rows = 8 * RW;
-  k_pair<RW, D, OP, MB><<<unsigned((p.na + rows - 1) / rows), kPcThreads, 0, st>>>(p);
+  constexpr bool kSepOp = OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART || OP == OTN_PC_LSE_SHIFT ||
+                          OP == OTN_PC_DOT || OP == OTN_PC_DIAG;
+  if (kSepOp && sep && p.cmax > 0.0)
+    k_pair<RW, D, OP, MB, kSepOp><<<unsigned((p.na + rows - 1) / rows), kPcThreads, 0, st>>>(p);
+  else
+    k_pair<RW, D, OP, MB, false><<<unsigned((p.na + rows - 1) / rows), kPcThreads, 0, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -218,34 +271,34 @@ static cudaError_t launch_rw(const PairArgs& p, cudaStream_t st) {
 // when that leaves SMs idle.  8 rows per warp spills (the previous choice,
 // 1.6-1.8x slower).
 template <int D, int OP>
-static cudaError_t launch_d(const PairArgs& p, cudaStream_t st, int num_sms) {
+static cudaError_t launch_d(const PairArgs& p, cudaStream_t st, int num_sms, bool sep) {
   if (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART || OP == OTN_PC_LSE_SHIFT ||
       (p.na + 31) / 32 < num_sms)
-    return launch_rw<2, D, OP, 3>(p, st);
-  return launch_rw<4, D, OP, 2>(p, st);
+    return launch_rw<2, D, OP, 3>(p, st, sep);
+  return launch_rw<4, D, OP, 2>(p, st, sep);
 }
 
 template <int OP>
-static cudaError_t launch_pair_op(const PairArgs& p, cudaStream_t st, int num_sms) {
+static cudaError_t launch_pair_op(const PairArgs& p, cudaStream_t st, int num_sms, bool sep) {
   switch (p.d) {
-    case 1: return launch_d<1, OP>(p, st, num_sms);
-    case 2: return launch_d<2, OP>(p, st, num_sms);
-    case 3: return launch_d<3, OP>(p, st, num_sms);
-    case 4: return launch_d<4, OP>(p, st, num_sms);
+    case 1: return launch_d<1, OP>(p, st, num_sms, sep);
+    case 2: return launch_d<2, OP>(p, st, num_sms, sep);
+    case 3: return launch_d<3, OP>(p, st, num_sms, sep);
+    case 4: return launch_d<4, OP>(p, st, num_sms, sep);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_pair(otn_ctx* x, const PairArgs& p) {
   switch (p.op) {
-    case OTN_PC_LSE: return launch_pair_op<OTN_PC_LSE>(p, x->stream, x->num_sms);
-    case OTN_PC_DOT: return launch_pair_op<OTN_PC_DOT>(p, x->stream, x->num_sms);
-    case OTN_PC_DIAG: return launch_pair_op<OTN_PC_DIAG>(p, x->stream, x->num_sms);
-    case OTN_PC_MAXD: return launch_pair_op<OTN_PC_MAXD>(p, x->stream, x->num_sms);
-    case OTN_PC_LSE_PART: return launch_pair_op<OTN_PC_LSE_PART>(p, x->stream, x->num_sms);
-    case OTN_PC_DOTC: return launch_pair_op<OTN_PC_DOTC>(p, x->stream, x->num_sms);
-    case OTN_PC_CDOT: return launch_pair_op<OTN_PC_CDOT>(p, x->stream, x->num_sms);
-    case OTN_PC_LSE_SHIFT: return launch_pair_op<OTN_PC_LSE_SHIFT>(p, x->stream, x->num_sms);
+    case OTN_PC_LSE: return launch_pair_op<OTN_PC_LSE>(p, x->stream, x->num_sms, !x->pc_exact);
+    case OTN_PC_DOT: return launch_pair_op<OTN_PC_DOT>(p, x->stream, x->num_sms, !x->pc_exact);
+    case OTN_PC_DIAG: return launch_pair_op<OTN_PC_DIAG>(p, x->stream, x->num_sms, !x->pc_exact);
+    case OTN_PC_MAXD: return launch_pair_op<OTN_PC_MAXD>(p, x->stream, x->num_sms, !x->pc_exact);
+    case OTN_PC_LSE_PART: return launch_pair_op<OTN_PC_LSE_PART>(p, x->stream, x->num_sms, !x->pc_exact);
+    case OTN_PC_DOTC: return launch_pair_op<OTN_PC_DOTC>(p, x->stream, x->num_sms, !x->pc_exact);
+    case OTN_PC_CDOT: return launch_pair_op<OTN_PC_CDOT>(p, x->stream, x->num_sms, !x->pc_exact);
+    case OTN_PC_LSE_SHIFT: return launch_pair_op<OTN_PC_LSE_SHIFT>(p, x->stream, x->num_sms, !x->pc_exact);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -86,3 +86,36 @@ def test_otf_cost_bitwise(n, d, scale):
         cost.pass_(_lib.PC_CDOT, rows_first=True, out=out, vec=e)
         got = out.cpu().numpy()
         np.testing.assert_array_equal(got.view(np.int64), C[:, k].view(np.int64))
+
+
+def test_separable_exponent_matches_exact_cost_path():
+    """The separable plan exponent of the on-the-fly exp passes (the default)
+    against the exact-cost path (OTN_PC_EXACT=1, read when a context is
+    created: a fresh process): same trajectory, potentials within 1e-11."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import json, sys
+sys.path.insert(0, ".")
+from paper_2504_02067_b200 import mdot, problems
+pc = problems.points_problem(2048, 3, 4)
+sol = mdot(pc, 2.0 ** 5, 2.0 ** 11)
+st = sol.final_state
+print(json.dumps(dict(u=st.u.tolist(), v=st.v.tolist(), primal=sol.primal_cost,
+                      cg=[it.stats.cg_iters for it in sol.iterations])))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = []
+    for exact in ("0", "1"):
+        out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True,
+                             text=True, env=dict(os.environ, OTN_PC_EXACT=exact), timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        runs.append(json.loads(out.stdout.strip().splitlines()[-1]))
+    sep, exact = runs
+    assert sep["cg"] == exact["cg"]
+    for k in ("u", "v"):
+        a, b = np.array(sep[k]), np.array(exact[k])
+        assert np.abs(a - b).max() <= 1e-11 * np.abs(b).max()
+    assert sep["primal"] == pytest.approx(exact["primal"], rel=1e-11)
