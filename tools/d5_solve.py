@@ -35,4 +35,4 @@ res = {"n": n, "dim": 3, "gamma": [2.0 ** 5, 2.0 ** lg], "gpus": 1, "solve_s": d
                       "wall_ms": it.wall_ms} for it in sol.iterations]}
 print(json.dumps(res, indent=1))
 os.makedirs("gpurun_out", exist_ok=True)
-json.dump(res, open("gpurun_out/r01_d5_solve.json", "w"), indent=1)
+json.dump(res, open(os.environ.get("D5_OUT", "gpurun_out/r02_d5_solve.json"), "w"), indent=1)
