@@ -400,6 +400,7 @@ def d4_solve(dev, n, comm=None):
     dt = time.perf_counter() - t0
     collectives = {k: v - before.get(k, 0) for k, v in comm.stats.items()}
     passes = TELEMETRY.calls.get("otn_pc_pass", 0)
+    launches = TELEMETRY.launches
     st = sol.final_state
     st.set_targets(pc.r, pc.c)
     err = st.grad_norm_l1()
@@ -408,7 +409,8 @@ def d4_solve(dev, n, comm=None):
     rec = {"n": n, "dim": 3, "gamma": list(D4_GAMMA), "gpus": comm.world,
            "sharding": f"rows over {comm.world} ranks" if comm.world > 1 else "none",
            "stages": len(sol.iterations), "cg": sum(i.stats.cg_iters for i in sol.iterations),
-           "passes_per_rank": passes, "true_marginal_err": err, "primal": sol.primal_cost,
+           "passes_per_rank": passes, "launches_per_rank": launches,
+           "true_marginal_err": err, "primal": sol.primal_cost,
            "collectives": collectives,
            "entries_per_s_per_gpu": entries / dt,
            "fp64_pipe_frac_est": entries / dt / peak_entries,
@@ -463,7 +465,7 @@ def run_sharded(args, rank, world, dev):
     n = 2 ** 20 if args.sharded == "d5" else (args.d4_n or 65536)
     out_extras = {}
     # the 1-GPU reference solve of the same n on rank 0 (strong-scaling basis;
-    # D5 on one GPU takes ~10 min: profiles/r01_d5_solve.json instead)
+    # D5 on one GPU takes ~7 min: profiles/r02_d5_solve.json instead)
     if rank == 0 and not args.no_extras and n <= 2 ** 17:
         dt1, rec1 = d4_solve(dev, n, comm=Comm.local())
         rec1["s"] = dt1
@@ -471,11 +473,12 @@ def run_sharded(args, rank, world, dev):
     comm.barrier()
     for _ in range(min(args.warmup, 1)):                  # a D4 solve is seconds: one warm-up
         d4_solve(dev, n, comm)
-    times, rec = [], None
+    times, rec, launches = [], None, 0
     with ClockSampler(dev.index) as clocks:
         for _ in range(args.steps):
             dt, rec = d4_solve(dev, n, comm)
             times.append(max_over_ranks(dt, world))
+            launches += rec["launches_per_rank"]
     TELEMETRY.reset()
     # e2e: the same public call with the points built on the host inside the
     # timed region (H2D of the row shard + all column points; D2H of the result)
@@ -486,7 +489,7 @@ def run_sharded(args, rank, world, dev):
     _ = sol.primal_cost
     torch.cuda.synchronize()
     e2e = max_over_ranks(time.perf_counter() - t0, world)
-    h2d = TELEMETRY.h2d
+    h2d, d2h = TELEMETRY.h2d, TELEMETRY.d2h
     if not args.no_extras:
         out_extras["d2_replicas"] = d2_replicas(dev, rank, world)
     val = statistics.mean(times)
@@ -497,8 +500,9 @@ def run_sharded(args, rank, world, dev):
         "data": "synthetic (seeded U[0,1)^3 point clouds, uniform marginals)",
         "config": config_d4(n, world),
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": 8},
-        "gpu_launches": None,
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches / max(args.steps, 1),
         "solve": rec, "per_step_s": times, "clocks": clocks.summary(),
         "collectives": {"backend": _BACKEND, "ranks": world,
                         "per_solve": rec.get("collectives")},

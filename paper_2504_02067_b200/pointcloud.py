@@ -141,6 +141,7 @@ class CudaBackend:
         fl = ctypes.c_int(0)
         self.ctx.call("otn_reduce_n", int(n), int(op), vptr(a), vptr(b), vptr(c), vptr(d), out,
                       ctypes.byref(fl))
+        TELEMETRY.d2h += 20                     # two sums and the flag word
         return float(out[0]), float(out[1]), int(fl.value)
 
     def reduce_dev(self, n, op, dst, a, b=None, c=None, d=None):
@@ -228,6 +229,7 @@ class PointCloudCost:
         view = buf[: 2 * len(items)]
         self.comm.sum_(view, "scalar_allreduces")
         vals = view.tolist()
+        TELEMETRY.d2h += 16 * len(items)
         return [(vals[2 * k], vals[2 * k + 1]) for k in range(len(items))]
 
     def zeros(self, n):
