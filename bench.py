@@ -442,6 +442,24 @@ def run_extras(args, dev):
                            "stages": len(sol.iterations),
                            "cg": sum(i.stats.cg_iters for i in sol.iterations),
                            "true_marginal_err": st.grad_norm_l1()}
+        # the median over seeds 0..4 (L2^2) and the L1 cost
+        seeds = []
+        for spec in [f"grid:64:l2sq:{s}" for s in range(5)] + ["grid:64:l1:0"]:
+            p = ot.workload(spec)
+            dp = ot.Problem(C=torch.from_numpy(p.C).to(dev), r=p.r, c=p.c)
+            ot.mdot(dp, D2["gamma_i"], D2["gamma_f"])
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            sol = ot.mdot(dp, D2["gamma_i"], D2["gamma_f"])
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            st = sol.final_state
+            st.set_targets(p.r, p.c)
+            seeds.append({"spec": spec, "s": dt, "stages": len(sol.iterations),
+                          "cg": sum(i.stats.cg_iters for i in sol.iterations),
+                          "true_marginal_err": st.grad_norm_l1()})
+        l2 = sorted(x["s"] for x in seeds if "l2sq" in x["spec"])
+        extras["d2_seeds"] = {"runs": seeds, "l2sq_median_s": l2[len(l2) // 2]}
         extras["fused_px"] = fused_px(dev, float(peaks["hbm_gbs"]))
         if args.d4_n:
             dt, rec = d4_solve(dev, args.d4_n)
