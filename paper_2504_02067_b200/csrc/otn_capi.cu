@@ -99,6 +99,7 @@ otn::CoopArgs base_args(otn_ctx* x, const double* P) {
   a.sv = x->sv;
   a.wpart = x->wpart;
   a.red = x->red;
+  a.gs_epoch = x->gs_epoch;
   a.res = x->dres;
   return a;
 }
@@ -175,7 +176,8 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
   size_t o_t0 = off; off += vec;
   size_t o_t1 = off; off += vec;
   size_t o_wp = off; off += align_up(size_t(x->coop_blocks) * ld * sizeof(double), 256);
-  size_t o_red = off; off += align_up(size_t(otn::kRedSlots) * otn::kRedStride * otn::kRedWidth * sizeof(double), 256);
+  size_t o_red = off; off += align_up(size_t(otn::kRedSlots) * otn::kRedStride * otn::kRedWidth * 16, 256);
+  size_t o_gse = off; off += 256;
   size_t o_lse = off; off += align_up(size_t(x->lse_slabs) * ld * 2 * sizeof(double), 256);
   {
     // the bulk-copy row LSE is opt-in (OTN_LSE_BULK=1): measured slower than
@@ -215,6 +217,7 @@ int otn_create(otn_ctx** out, int device, int64_t n, int64_t ld, void* stream) {
   x->vtmp1 = (double*)(base + o_t1);
   x->wpart = (double*)(base + o_wp);
   x->red = (double*)(base + o_red);
+  x->gs_epoch = (uint32_t*)(base + o_gse);
   x->lse_part = (double*)(base + o_lse);
 
   x->scal = (double*)(base + o_sc);

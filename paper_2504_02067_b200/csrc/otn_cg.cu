@@ -39,7 +39,6 @@ struct Smem {
   double a2[NW][33];
   double xs[NT];                    // phase A input: x of the CTA's rows (row - r0)
   double sv[NT];                    // phase B output: (P w) of the CTA's rows
-  double2 rbuf[2][kRedStride / 2];  // grid_reduce_begin/end: the G partials, fetched async
   double bp[NW][kRows];             // phase B: per-warp partial row dots
 };
 
@@ -47,116 +46,88 @@ __device__ __forceinline__ double2 ldcg2(const double* p) {
   return __ldcg(reinterpret_cast<const double2*>(p));
 }
 
-// Deterministic grid-wide sum of K values: fixed warp / block / grid trees.
-// Value k is reduced by warp k (in parallel); one grid barrier; then every CTA
-// reads the G partials of value k with a few 16-byte loads (layout
-// [slot][k][kRedStride]: contiguous per value).  Slots rotate so a fast CTA
-// never overwrites partials a slow CTA is still reading.  (Measured: ~3.4 us
-// per reduce vs ~1.5 us for a bare grid.sync(); the extra is the store ->
-// barrier -> load round trip of the partials: replicating them to spread the
-// readers over more L2 lines, or a last-arriver reduction, did not help.)
-template <int K>
-__device__ __forceinline__ void grid_reduce(cg::grid_group& grid, double (&v)[K], double* red,
-                                            int& slot, Smem& sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int G = gridDim.x;
-  double* base = red + int64_t(slot) * kRedWidth * kRedStride;
-#pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) sh.red[k][warp] = v[k];
-  }
-  __syncthreads();
-  if (warp < K) {
-    const double t = warp_sum(lane < NW ? sh.red[warp][lane] : 0.0);
-    if (lane == 0) base[warp * kRedStride + blockIdx.x] = t;
-  }
-  grid.sync();
-  if (warp < K) {
-    const double* src = base + warp * kRedStride;
-    double2 part[kRedStride / 64];
-#pragma unroll
-    for (int m = 0; m < kRedStride / 64; ++m) {
-      const int b = 64 * m + 2 * lane;
-      part[m] = b < G ? ldcg2(src + b) : make_double2(0.0, 0.0);
-      if (b + 1 == G) part[m].y = 0.0;              // odd G: the pair's second slot is not a CTA
-    }
-    double t = 0.0;
-#pragma unroll
-    for (int m = 0; m < kRedStride / 64; ++m) t += part[m].x + part[m].y;
-    t = warp_sum(t);
-    if (lane == 0) sh.gres[warp] = t;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = sh.gres[k];
-  slot ^= 1;
-}
+// Grid-wide barrier and deterministic sum of K values in one exchange.
+//
+// Every CTA reduces value k with warp k (fixed warp / block trees) and stores
+// the CTA total into its slot of row k; thread 0 then arrives on the
+// context's arrival counter (release) and spins until the counter reaches
+// e * G for this exchange's epoch e (acquire); warp k reads the G totals of
+// row k and sums them in a fixed order.  The counter and the epoch only ever
+// increase (the last epoch is carried to the next launch, a.gs_epoch), so
+// the counter is never reset; two slot sets alternate, so a fast CTA's next
+// store never lands on a slot a slow CTA is still reading.  K = 0: barrier
+// only.  Measured (tools/gsync_bench.cu, 148 x 512 threads): 2.06 us per
+// 2-value exchange vs 3.61 us for cooperative groups' grid.sync() followed by
+// the same loads (the bare barriers cost the same, 1.3 us).
+// Summation order: lane l holds CTAs 64 m + 2 l + {0, 1}; sum over m of the
+// pair sums, then the warp butterfly.
+__shared__ uint32_t s_ep;                           // last completed exchange (written by thread 0)
 
-// The same reduction split around independent work: grid_reduce_begin does
-// the barrier and starts copying the G partials into shared memory
-// (cp.async, zero-filled past G); grid_reduce_end waits for them and sums in
-// the same fixed order.  Whatever runs in between (phase B of the HVP) hides
-// the partials' load latency.  K <= 2.
-__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-               "r"(valid ? 16 : 0) : "memory");
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
+// the arrival counter sits one 128-byte line after the epoch word
+__device__ __forceinline__ uint32_t* gs_counter(const CoopArgs& a) { return a.gs_epoch + 32; }
 
 template <int K>
-__device__ __forceinline__ void grid_reduce_begin(cg::grid_group& grid, double (&v)[K], double* red,
-                                                  int slot, Smem& sh) {
-  static_assert(K <= 2, "rbuf holds two values");
+__device__ __forceinline__ void gs_exchange(const CoopArgs& a, double* v, Smem& sh) {
+  constexpr int M = kRedStride / 64;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = gridDim.x;
-  double* base = red + int64_t(slot) * kRedWidth * kRedStride;
+  const uint32_t e = s_ep + 1u;
+  double* row = a.red + (size_t(e & 1u) * kRedWidth + warp) * kRedStride;
+  if (K > 0) {
 #pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
-  if (lane == 0) {
+    for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+    if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) sh.red[k][warp] = v[k];
+      for (int k = 0; k < K; ++k) sh.red[k][warp] = v[k];
+    }
+    __syncthreads();
+    if (warp < K) {
+      const double t = warp_sum(lane < NW ? sh.red[warp][lane] : 0.0);
+      if (lane == 0) __stcg(row + blockIdx.x, t);
+    }
   }
   __syncthreads();
-  if (warp < K) {
-    const double t = warp_sum(lane < NW ? sh.red[warp][lane] : 0.0);
-    if (lane == 0) base[warp * kRedStride + blockIdx.x] = t;
-  }
-  grid.sync();
-  if (warp < K) {
-    const double* src = base + warp * kRedStride;
-#pragma unroll
-    for (int m = 0; m < kRedStride / 64; ++m) {
-      const int b = 64 * m + 2 * lane;
-      cp_async16_zfill(static_cast<uint32_t>(__cvta_generic_to_shared(&sh.rbuf[warp][32 * m + lane])),
-                       src + (b < G ? b : 0), b < G);
+  if (threadIdx.x == 0) {
+    uint32_t* cnt = gs_counter(a);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    const uint32_t target = e * uint32_t(G);
+    while (int32_t(ld_acquire_u32(cnt) - target) < 0) {
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
+    s_ep = e;                                       // read again only after the next barrier
+  }
+  __syncthreads();
+  if (K > 0) {
+    if (warp < K) {
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const int b = 64 * m + 2 * lane;
+        double2 pr = b < G ? ldcg2(row + b) : make_double2(0.0, 0.0);
+        if (b + 1 == G) pr.y = 0.0;                 // odd G: the pair's second slot is not a CTA
+        s += pr.x + pr.y;
+      }
+      s = warp_sum(s);
+      if (lane == 0) sh.gres[warp] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = sh.gres[k];
   }
 }
 
 template <int K>
-__device__ __forceinline__ void grid_reduce_end(double (&v)[K], int& slot, Smem& sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int G = gridDim.x;
-  if (warp < K) {
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncwarp();
-    double t = 0.0;
-#pragma unroll
-    for (int m = 0; m < kRedStride / 64; ++m) {
-      const int b = 64 * m + 2 * lane;
-      double2 pr = sh.rbuf[warp][32 * m + lane];
-      if (b + 1 == G) pr.y = 0.0;                   // odd G: the pair's second slot is not a CTA
-      t += pr.x + pr.y;
-    }
-    t = warp_sum(t);
-    if (lane == 0) sh.gres[warp] = t;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = sh.gres[k];
-  slot ^= 1;
+__device__ __forceinline__ void grid_reduce(double (&v)[K], const CoopArgs& a, Smem& sh) {
+  gs_exchange<K>(a, v, sh);
+}
+
+// Grid barrier (no values).
+__device__ __forceinline__ void grid_bar(const CoopArgs& a, Smem& sh) {
+  gs_exchange<0>(a, nullptr, sh);
 }
 
 // ---------------------------------------------------------------------------
@@ -1012,9 +983,9 @@ __device__ double hvp(cg::grid_group& grid, const CoopArgs& a, double xv, double
     ++nh;
     stage_x(xv, sh);
     phase_a(plan_view(a, r0, r1), r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
-    grid.sync();
+    grid_bar(a, sh);
     phase_a2(a, 0, a.wc, sh);
-    grid.sync();
+    grid_bar(a, sh);
     phase_b(plan_view(a, r0, r1), a.wc, r0, r1, sh);   // ends with a barrier
     if (int64_t(threadIdx.x) < r1 - r0) o = __dsub_rn(o, __dmul_rn(rho, sh.sv[threadIdx.x]));
     else o = 0.0;                                   // no row: sh.sv is not written there
@@ -1043,7 +1014,7 @@ struct PcgOut {
 // the matvec part of p.q are formed by linearity.
 __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, double rPi, double rho,
                       const double* bvec, double tol, double& x, bool has_x0, int64_t max_iters,
-                      int64_t r0, int64_t r1, int& slot, Smem& sh, int64_t& nh) {
+                      int64_t r0, int64_t r1, Smem& sh, int64_t& nh) {
   PcgOut o{OTN_OK, 0, 0.0};
   const bool mv = rho != 0.0;                       // F(0) = diag(rP): no plan passes
   double q = 0.0;
@@ -1072,7 +1043,7 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
     stage_x(p, sh);
     phase_a(plan_view(a, r0, r1), r0, r1, wrow, sh);
   }
-  grid_reduce<3>(grid, loc, a.red, slot, sh);
+  grid_reduce<3>(loc, a, sh);
   if (loc[2] > 0.0) { o.status = OTN_ST_PRECOND; return o; }
   if (loc[0] <= tol) { o.resid = loc[0]; return o; }
   double rz = loc[1];
@@ -1094,9 +1065,9 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
     // between A2 and phase B (one barrier fewer than p.q after phase B).
     double wq = 0.0;
     if (pending) {
-      // finish the previous iteration's r.z reduction under A2's partial loads
+      // the previous iteration's r.z exchange is complete (nz holds the sums)
       a2_sums(a, sh);
-      grid_reduce_end<2>(nz, slot, sh);             // its closing barrier publishes sh.a2
+      __syncthreads();                              // publishes sh.a2
       pending = false;
       norm = nz[0];
       if (norm <= tol) { o.iters = k - 1; o.resid = norm; return o; }
@@ -1115,14 +1086,13 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
         if (split && slice_lane) wreg = __ldcg(a.q + slice_j);   // just written by this thread
       }
       double sums[2] = {fma(p, q, 0.0), wq};
-      grid_reduce_begin<2>(grid, sums, a.red, slot, sh);
+      grid_reduce<2>(sums, a, sh);             // also publishes a.wc
       phase_b(plan_view(a, r0, r1), a.wc, r0, r1, sh);   // ends with a barrier
-      grid_reduce_end<2>(sums, slot, sh);
       pq = __dsub_rn(sums[0], __dmul_rn(rho, sums[1]));
       q = row.own ? __dsub_rn(q, __dmul_rn(rho, sh.sv[threadIdx.x])) : 0.0;
     } else {
       double pq1[1] = {fma(p, q, 0.0)};
-      grid_reduce<1>(grid, pq1, a.red, slot, sh);
+      grid_reduce<1>(pq1, a, sh);
       pq = pq1[0];
     }
     fresh = false;
@@ -1143,11 +1113,11 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
     nz[0] = fabs(r);
     nz[1] = fma(r, z, 0.0);
     if (split) {
-      grid_reduce_begin<2>(grid, nz, a.red, slot, sh);
+      grid_reduce<2>(nz, a, sh);
       pending = true;
       continue;                                     // finished at the top of the next iteration
     }
-    grid_reduce<2>(grid, nz, a.red, slot, sh);
+    grid_reduce<2>(nz, a, sh);
     norm = nz[0];
     if (norm <= tol) { o.iters = k; o.resid = norm; return o; }
     beta = nz[1] / rz;
@@ -1155,7 +1125,7 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
     rz = nz[1];
   }
   if (pending) {                                    // the budget ran out on a begun reduction
-    grid_reduce_end<2>(nz, slot, sh);
+    // (nz was completed by its exchange)
     norm = nz[0];
     if (norm <= tol) { o.iters = max_iters; o.resid = norm; return o; }
   }
@@ -1170,7 +1140,7 @@ __device__ void column_pass(cg::grid_group& grid, const CoopArgs& a, double xv, 
                             double* out, int64_t r0, int64_t r1, Smem& sh) {
   stage_x(xv, sh);
   phase_a(plan_view(a, r0, r1), r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
-  grid.sync();
+  grid_bar(a, sh);
   phase_a2(a, kind, out, sh);
 }
 
@@ -1190,8 +1160,10 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
   const int G = gridDim.x;
   const int64_t r0 = a.part[blockIdx.x];             // rows [r0, r1): k_partition
   const int64_t r1 = a.part[blockIdx.x + 1];
-  if (threadIdx.x == 0) s_mode = a.part[G + 1];
-  int slot = 0;
+  if (threadIdx.x == 0) {
+    s_mode = a.part[G + 1];
+    s_ep = *reinterpret_cast<volatile const uint32_t*>(a.gs_epoch);   // the previous launch's last
+  }
   int64_t nh = 0;
   DevResult res{};
   res.status = OTN_OK;
@@ -1217,7 +1189,7 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
   if (a.mode == kModeNewton) {
     const double gi = row.own ? __ldg(a.g + row.i) : 0.0;
     double gl[1] = {fabs(gi)};
-    grid_reduce<1>(grid, gl, a.red, slot, sh);
+    grid_reduce<1>(gl, a, sh);
     const double gn = gl[0];
     res.rho_final = a.rho0;
     double d = 0.0;
@@ -1230,7 +1202,7 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
       while (true) {
         const double q = hvp(grid, a, d, 1.0, rPi, r0, r1, sh, nh);
         double rl[1] = {row.own ? fabs(__dadd_rn(q, gi)) : 0.0};
-        grid_reduce<1>(grid, rl, a.red, slot, sh);
+        grid_reduce<1>(rl, a, sh);
         if (rl[0] <= target) { res.resid_l1 = rl[0]; break; }
         if (__dsub_rn(1.0, rho) < 1e-12) {
           res.status = OTN_ST_STAGNATION;
@@ -1240,7 +1212,7 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
         }
         ++res.pcg_calls;
         const PcgOut po = pcg(grid, a, row, rPi, rho, nullptr, tol, d, a.zero_init == 0,
-                              a.max_iters, r0, r1, slot, sh, nh);
+                              a.max_iters, r0, r1, sh, nh);
         if (po.status != OTN_OK) {
           res.status = po.status;
           res.diag_rho = rho;
@@ -1259,14 +1231,14 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
     if (res.status == OTN_OK && a.dv) {
       column_pass(grid, a, d, 1, a.dv, r0, r1, sh);
       double sl[1] = {fma(gi, d, 0.0)};
-      grid_reduce<1>(grid, sl, a.red, slot, sh);
+      grid_reduce<1>(sl, a, sh);
       res.slope = -sl[0];
     }
   } else if (a.mode == kModePcg) {
     res.pcg_calls = 1;
     double x = row.own && a.has_x0 ? a.d[row.i] : 0.0;
     const PcgOut po = pcg(grid, a, row, rPi, a.rho, a.b, a.tol, x, a.has_x0 != 0, a.max_iters,
-                          r0, r1, slot, sh, nh);
+                          r0, r1, sh, nh);
     if (row.own) a.d[row.i] = x;
     res.status = po.status;
     res.cg_iters = po.iters;
@@ -1278,7 +1250,7 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
     if (row.own) a.d[row.i] = q;
   } else if (a.mode == kModePc || a.mode == kModeRmatvec) {
     column_pass(grid, a, row.own ? a.xin[row.i] : 0.0, a.mode == kModePc ? 0 : 2, a.wc, r0, r1, sh);
-    grid.sync();
+    grid_bar(a, sh);
     for (int64_t i = int64_t(blockIdx.x) * NT + threadIdx.x; i < a.n; i += int64_t(G) * NT)
       a.d[i] = __ldcg(a.wc + i);
   } else if (a.mode == kModeProbe) {
@@ -1288,10 +1260,10 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
     stage_x(xv, sh);
     for (int64_t k = 0; k < a.max_iters; ++k) {
       if (what == 0) {
-        grid.sync();
+        grid_bar(a, sh);
       } else if (what == 1) {
         double v[2] = {1.0, 2.0};
-        grid_reduce<2>(grid, v, a.red, slot, sh);
+        grid_reduce<2>(v, a, sh);
       } else if (what == 2) {
         phase_a(plan_view(a, r0, r1), r0, r1, a.wpart + int64_t(blockIdx.x) * a.ld, sh);
         __syncthreads();
@@ -1299,7 +1271,7 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
         phase_b(plan_view(a, r0, r1), a.xin, r0, r1, sh);
       } else if (what == 4) {
         column_pass(grid, a, xv, 0, a.wc, r0, r1, sh);
-        grid.sync();
+        grid_bar(a, sh);
       } else {
         const double q = hvp(grid, a, xv, 0.5, rPi, r0, r1, sh, nh);
         if (row.own) a.d[row.i] = q;
@@ -1309,7 +1281,7 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
     // stage x into the padded workspace vector (phase B reads ld entries)
     for (int64_t j = int64_t(blockIdx.x) * NT + threadIdx.x; j < a.ld; j += int64_t(G) * NT)
       a.wc[j] = j < a.n ? __ldg(a.xin + j) : 0.0;
-    grid.sync();
+    grid_bar(a, sh);
     phase_b(plan_view(a, r0, r1), a.wc, r0, r1, sh);
     if (row.own) a.d[row.i] = sh.sv[threadIdx.x];
   }
@@ -1322,6 +1294,7 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
     int rmax = 0;
     for (int b = 0; b < G; ++b) rmax = max(rmax, a.part[b + 1] - a.part[b]);
     res.plan_rows_max = rmax;
+    *a.gs_epoch = s_ep;                             // this thread completed the last exchange
     publish_result(a, res);
   }
 }

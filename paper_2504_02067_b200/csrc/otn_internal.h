@@ -48,7 +48,8 @@ struct otn_ctx {
   size_t ws_bytes;
   double *r, *z, *p, *q, *M, *wc, *sv, *vtmp0, *vtmp1;   // length ld each
   double* wpart;          // coop_blocks x ld column partials
-  double* red;            // kRedSlots x coop_blocks x kRedWidth grid-reduction partials
+  double* red;            // grid-exchange slots: kRedSlots x kRedWidth x kRedStride x 16 B
+  uint32_t* gs_epoch;     // last grid-exchange epoch (k_coop reads it at start, writes at exit)
   double* lse_part;       // lse_slabs x ld x 2 (m, s) column-LSE partials
   int lse_bulk_ctas;      // persistent CTAs of the bulk-copy row LSE (0: register streaming)
   int cfg_err;            // first error while configuring optional kernels (diagnostic)
@@ -110,7 +111,9 @@ struct CoopArgs {
   const int* part;        // row partition + plan mode (k_partition, set by launch_coop)
   void* sg;               // compressed-rows buffer of kPlanSparseG (nullable; set by launch_coop)
   // workspace
-  double *r, *z, *p, *q, *M, *wc, *sv, *wpart, *red;
+  double *r, *z, *p, *q, *M, *wc, *sv, *wpart;
+  double* red;            // grid exchange slots (k_coop gs_exchange: 2 x kRedWidth x kRedStride x 16 B)
+  uint32_t* gs_epoch;     // last grid-exchange epoch of the context
   DevResult* res;
   int* step_flags;        // nullable: otn_newton_step's gate words (see k_step_gate stage 0)
 };

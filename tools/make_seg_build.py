@@ -39,8 +39,8 @@ rep('''      a2_sums(a, sh);
       SEG(1);
       grid_reduce_end<2>(nz, slot, sh);
       SEG(2);''')
-rep('''      wq = a2_tail(a, a.wc, sh, fresh ? nullptr : a.q, beta, a.q);
-    }''', '''      wq = a2_tail(a, a.wc, sh, fresh ? nullptr : a.q, beta, a.q);
+rep('''      wq = a2_tail(a, a.wc, sh, beta, wreg, cPj);
+    }''', '''      wq = a2_tail(a, a.wc, sh, beta, wreg, cPj);
       SEG(3);
     }''')
 rep('''      grid_reduce_begin<2>(grid, sums, a.red, slot, sh);
