@@ -1106,13 +1106,18 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
     }
     if (!row.own) r = 0.0;
     z = __ddiv_rn(r, M);
-    if (mv) {                                       // partials of z, read after the barrier
+    // With the true residual (every kRefresh iterations) P^T p is re-anchored
+    // too: the next direction's column sums are formed directly instead of by
+    // the recurrence P^T z + beta P^T p, whose rounding drifts over long CG
+    // runs (residual replacement; the partials of z are not needed then).
+    const bool anchor = mv && k % kRefresh == 0;
+    if (mv && !anchor) {                            // partials of z, read after the barrier
       stage_x(z, sh);
       phase_a(plan_view(a, r0, r1), r0, r1, wrow, sh);
     }
     nz[0] = fabs(r);
     nz[1] = fma(r, z, 0.0);
-    if (split) {
+    if (split && !anchor) {
       grid_reduce<2>(nz, a, sh);
       pending = true;
       continue;                                     // finished at the top of the next iteration
@@ -1123,6 +1128,12 @@ __device__ PcgOut pcg(cg::grid_group& grid, const CoopArgs& a, const Row& row, d
     beta = nz[1] / rz;
     p = __dadd_rn(z, __dmul_rn(beta, p));
     rz = nz[1];
+    if (anchor) {                                   // partials of p itself; A2 sums them directly
+      stage_x(p, sh);
+      phase_a(plan_view(a, r0, r1), r0, r1, wrow, sh);
+      grid_bar(a, sh);
+      fresh = true;
+    }
   }
   if (pending) {                                    // the budget ran out on a begun reduction
     // (nz was completed by its exchange)

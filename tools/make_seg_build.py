@@ -35,22 +35,19 @@ rep('''  for (int64_t k = 1; k <= max_iters; ++k) {
     SEG(0);
     // p.q = sum_i rP_i p_i^2''')
 rep('''      a2_sums(a, sh);
-      grid_reduce_end<2>(nz, slot, sh);''', '''      a2_sums(a, sh);
+      __syncthreads();                              // publishes sh.a2''', '''      a2_sums(a, sh);
       SEG(1);
-      grid_reduce_end<2>(nz, slot, sh);
+      __syncthreads();                              // publishes sh.a2
       SEG(2);''')
 rep('''      wq = a2_tail(a, a.wc, sh, beta, wreg, cPj);
     }''', '''      wq = a2_tail(a, a.wc, sh, beta, wreg, cPj);
       SEG(3);
     }''')
-rep('''      grid_reduce_begin<2>(grid, sums, a.red, slot, sh);
-      phase_b(plan_view(a, r0, r1), a.wc, r0, r1, sh);   // ends with a barrier
-      grid_reduce_end<2>(sums, slot, sh);''', '''      grid_reduce_begin<2>(grid, sums, a.red, slot, sh);
+rep('''      grid_reduce<2>(sums, a, sh);             // also publishes a.wc
+      phase_b(plan_view(a, r0, r1), a.wc, r0, r1, sh);   // ends with a barrier''', '''      grid_reduce<2>(sums, a, sh);             // also publishes a.wc
       SEG(4);
       phase_b(plan_view(a, r0, r1), a.wc, r0, r1, sh);   // ends with a barrier
-      SEG(5);
-      grid_reduce_end<2>(sums, slot, sh);
-      SEG(6);''')
+      SEG(5);''')
 rep('''    if (mv) {                                       // partials of z, read after the barrier
       stage_x(z, sh);
       phase_a(plan_view(a, r0, r1), r0, r1, wrow, sh);
@@ -61,8 +58,8 @@ rep('''    if (mv) {                                       // partials of z, rea
       phase_a(plan_view(a, r0, r1), r0, r1, wrow, sh);
       SEG(9);
     }''')
-rep('''      grid_reduce_begin<2>(grid, nz, a.red, slot, sh);
-      pending = true;''', '''      grid_reduce_begin<2>(grid, nz, a.red, slot, sh);
+rep('''      grid_reduce<2>(nz, a, sh);
+      pending = true;''', '''      grid_reduce<2>(nz, a, sh);
       SEG(10);
       pending = true;''')
 out = "/tmp/otn_cg_seg.cu"
