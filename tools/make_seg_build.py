@@ -48,20 +48,56 @@ rep('''      grid_reduce<2>(sums, a, sh);             // also publishes a.wc
       SEG(4);
       phase_b(plan_view(a, r0, r1), a.wc, r0, r1, sh);   // ends with a barrier
       SEG(5);''')
-rep('''    if (mv) {                                       // partials of z, read after the barrier
+rep('''    if (mv && !anchor) {                            // partials of z, read after the barrier
       stage_x(z, sh);
       phase_a(plan_view(a, r0, r1), r0, r1, wrow, sh);
     }''', '''    SEG(7);
-    if (mv) {                                       // partials of z, read after the barrier
+    if (mv && !anchor) {                            // partials of z, read after the barrier
       stage_x(z, sh);
       SEG(8);
       phase_a(plan_view(a, r0, r1), r0, r1, wrow, sh);
       SEG(9);
     }''')
-rep('''      grid_reduce<2>(nz, a, sh);
-      pending = true;''', '''      grid_reduce<2>(nz, a, sh);
+rep('''    if (split && !anchor) {
+      grid_reduce<2>(nz, a, sh);
+      pending = true;''', '''    if (split && !anchor) {
+      grid_reduce<2>(nz, a, sh);
       SEG(10);
       pending = true;''')
+# per-CTA work between exchanges and wait inside them (thread 0), per plan mode
+rep('''__shared__ uint32_t s_ep;''', '''__shared__ uint32_t s_ep;
+__shared__ long long s_tdone;
+__shared__ int s_dbgm;
+__device__ unsigned long long g_work[4][256], g_wait[4][256], g_nex[4][256];
+extern "C" int otn_dbg_cta(unsigned long long* host) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host, g_work, sizeof(g_work));
+  cudaMemcpyFromSymbol(host + 1024, g_wait, sizeof(g_wait));
+  cudaMemcpyFromSymbol(host + 2048, g_nex, sizeof(g_nex));
+  static unsigned long long z[4][256];
+  cudaMemcpyToSymbol(g_work, z, sizeof(z));
+  cudaMemcpyToSymbol(g_wait, z, sizeof(z));
+  cudaMemcpyToSymbol(g_nex, z, sizeof(z));
+  return 0;
+}''')
+rep('''    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    const uint32_t target = e * uint32_t(G);
+    while (int32_t(ld_acquire_u32(cnt) - target) < 0) {
+    }''', '''    const long long _ta = clock64();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    const uint32_t target = e * uint32_t(G);
+    while (int32_t(ld_acquire_u32(cnt) - target) < 0) {
+    }
+    const long long _td = clock64();
+    if (s_tdone != 0 && s_dbgm >= 0 && s_dbgm < 4) {
+      g_work[s_dbgm][blockIdx.x] += _ta - s_tdone;
+      g_wait[s_dbgm][blockIdx.x] += _td - _ta;
+      g_nex[s_dbgm][blockIdx.x] += 1;
+    }
+    s_tdone = _td;''')
+rep('''    s_mode = a.part[G + 1];''', '''    s_mode = a.part[G + 1];
+    s_tdone = 0;
+    s_dbgm = s_mode;''')
 out = "/tmp/otn_cg_seg.cu"
 open(out, "w").write(s)
 subprocess.check_call([os.path.join(ROOT, "tools/build_ab.sh"), "seg", out])

@@ -22,3 +22,23 @@ for m in (0, 2, 3):
     print(f"mode {m}: total {tot/1.965e3/1e3:.2f} ms  ({tot/1.965e3/hv[m]:.2f} us per hvp approx)")
     for i, nm in enumerate(names[:11]):
         print(f"   {nm:18s} {a[m][i]/1.965e3/hv[m]:7.2f} us/it")
+
+# per-CTA balance: work between exchanges vs wait inside them (thread 0 of every CTA)
+if hasattr(lib, "otn_dbg_cta"):
+    ot.mdot(dp, 2.0**5, 2.0**16)
+    cb = (ctypes.c_ulonglong * 3072)()
+    lib.otn_dbg_cta(cb)
+    sol = ot.mdot(dp, 2.0**5, 2.0**16)
+    lib.otn_dbg_cta(cb)
+    c = np.frombuffer(cb, dtype=np.uint64).reshape(3, 4, 256).astype(float)[:, :, :148]
+    for m in (0, 2, 3):
+        work, wait, nex = c[0][m], c[1][m], c[2][m]
+        if nex.max() == 0:
+            continue
+        ne = nex.max()
+        w = work / ne / 1.965e3
+        t = wait / ne / 1.965e3
+        print(f"mode {m}: {int(ne)} exchanges; work per exchange interval us: mean {w.mean():.2f} "
+              f"max {w.max():.2f} (CTA {int(w.argmax())}) min {w.min():.2f}; wait mean {t.mean():.2f} "
+              f"min {t.min():.2f}")
+        print("   slowest CTAs:", [(int(i), round(float(w[i]), 2)) for i in np.argsort(-w)[:6]])
