@@ -149,6 +149,16 @@ int otn_zero(otn_ctx* ctx, void* dst, int64_t bytes);
  * writes C^T (padding columns 0) for the column passes of an asymmetric C.  */
 int otn_is_symmetric(otn_ctx* ctx, const double* C, int* host_sym);
 int otn_transpose(otn_ctx* ctx, double* out, const double* C);
+/* Squared-Euclidean cost of 8-bit point sets on the tensor cores (K10, the
+ * setup GEMM of problems.py:87-111 for 784-d pixel sets): X, Y are n x d
+ * row-major float64 DEVICE arrays whose entries are integers in [0, 255];
+ * C (n x ld) := max(|x_i|^2 + |y_j|^2 - 2 x_i.y_j, 0) / (its maximum),
+ * padding columns 0.  The dot products run as exact u8 x u8 -> s32 MMAs, so
+ * C equals the host's float64 evaluation bit for bit.  host_max receives the
+ * maximum before normalization.  OTN_ERR_ARG when an entry is not an
+ * integer in [0, 255].  Synchronizes.                                        */
+int otn_pixel_cost(otn_ctx* ctx, const double* X, const double* Y, int64_t d, double* C,
+                   double* host_max);
 /* Synchronize and copy the four device status flags to the host:
  * [0] plan overflow, [1] nonpositive sums, [2] reduce domain, [3] rounding. */
 int otn_read_flags(otn_ctx* ctx, int* host4);

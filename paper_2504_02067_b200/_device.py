@@ -294,7 +294,11 @@ class DeviceCost:
         if is_tensor(C):
             if not C.is_cuda:
                 C = C.to(device)
-            if ld == self.n and C.is_contiguous():
+            padded = getattr(C, "_otn_padded", None)
+            if (padded is not None and padded.device == C.device and padded.data_ptr() == C.data_ptr()
+                    and tuple(padded.shape) == (self.n, ld)):
+                self.C = padded                  # built in the solver's layout (pixel_cost_device)
+            elif ld == self.n and C.is_contiguous():
                 self.C = C
             else:
                 self.C = self.ctx.zeros((self.n, ld))

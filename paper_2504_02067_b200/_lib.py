@@ -113,6 +113,7 @@ SIGNATURES = {
     "otn_zero": [_P, _P, _I64],
     "otn_is_symmetric": [_P, _P, _IP],
     "otn_transpose": [_P, _P, _P],
+    "otn_pixel_cost": [_P, _P, _P, _I64, _P, _DP],
     "otn_vec": [_P, _I, _D, _P, _P, _P, _P, _P],
     "otn_reduce": [_P, _I, _P, _P, _P, _P, _DP, _IP],
     "otn_row_stats": [_P, _P, _P, _P, _DP, _IP],

@@ -241,6 +241,7 @@ int otn_destroy(otn_ctx* x) {
   if (!x) return OTN_OK;
   if (x->ws) cudaFree(x->ws);
   if (x->sg) cudaFree(x->sg);
+  if (x->pix_scratch) cudaFree(x->pix_scratch);
   if (x->h_scal) cudaFreeHost(x->h_scal);
   if (x->h_flags) cudaFreeHost(x->h_flags);
   if (x->h_res) cudaFreeHost(x->h_res);
@@ -312,6 +313,24 @@ int otn_transpose(otn_ctx* x, double* out, const double* C) {
   DeviceGuard dg_(x);
   OTN_REQUIRE(x && out && C && out != C, "otn_transpose: bad argument");
   OTN_CUDA(otn::launch_transpose(x, out, C), "otn_transpose");
+  return OTN_OK;
+}
+
+int otn_pixel_cost(otn_ctx* x, const double* X, const double* Y, int64_t d, double* C,
+                   double* host_max) {
+  DeviceGuard dg_(x);
+  OTN_REQUIRE(x && X && Y && C && host_max, "otn_pixel_cost: NULL argument");
+  OTN_REQUIRE(d >= 1 && d <= (int64_t(1) << 15), "otn_pixel_cost: d must be in [1, 32768]");
+  // scratch words: the maximum's bits in scal[40], the range flag in flags[12]
+  unsigned long long* cmax_bits = reinterpret_cast<unsigned long long*>(x->scal + 40);
+  int* err = x->flags + 12;
+  OTN_CUDA(otn::launch_pixel_cost(x, X, Y, d, C, cmax_bits, err), "otn_pixel_cost");
+  int rc = sync_copy(x, x->h_scal + 40, x->scal + 40, sizeof(double), "otn_pixel_cost: max");
+  if (rc) return rc;
+  rc = sync_copy(x, x->h_flags + 12, x->flags + 12, sizeof(int), "otn_pixel_cost: flags");
+  if (rc) return rc;
+  OTN_REQUIRE(x->h_flags[12] == 0, "otn_pixel_cost: an entry is not an integer in [0, 255]");
+  *host_max = x->h_scal[40];
   return OTN_OK;
 }
 

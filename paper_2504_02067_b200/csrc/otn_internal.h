@@ -53,6 +53,8 @@ struct otn_ctx {
   double* lse_part;       // lse_slabs x ld x 2 (m, s) column-LSE partials
   int lse_bulk_ctas;      // persistent CTAs of the bulk-copy row LSE (0: register streaming)
   int cfg_err;            // first error while configuring optional kernels (diagnostic)
+  void* pix_scratch;      // otn_pixel_cost: packed u8 point sets + norms (grown on demand)
+  size_t pix_scratch_bytes;
   int pc_exact;           // on-the-fly passes: exact-cost exponent everywhere (OTN_PC_EXACT=1)
   double* scal;           // 64 device scalars
   int* flags;             // 16 device flag words
@@ -118,6 +120,9 @@ struct CoopArgs {
   int* step_flags;        // nullable: otn_newton_step's gate words (see k_step_gate stage 0)
 };
 cudaError_t launch_coop(otn_ctx* x, const CoopArgs& a);
+// K10 for 8-bit point sets (otn_pix.cu): C := squared distances / max, exact.
+cudaError_t launch_pixel_cost(otn_ctx* x, const double* X, const double* Y, int64_t d, double* C,
+                              unsigned long long* cmax_bits, int* err);
 size_t sparse_g_bytes_per_cta();        // kPlanSparseG buffer slice (allocated when ld <= 4096)
 
 // Vector kernels and single-CTA reductions.

@@ -20,6 +20,7 @@ this package's synthetic D1/D3/D4/D5 workloads.
 from __future__ import annotations
 
 import csv
+import ctypes
 from dataclasses import dataclass, fields
 
 import numpy as np
@@ -256,9 +257,49 @@ def points_problem(n, dim, seed, kind="uniform"):
     return PointCloudProblem(X=X, Y=Y, r=r, c=r.copy(), label=f"points{dim}-{kind}-n{n}-seed{seed}")
 
 
-def dense_points_problem(n, dim, seed, kind="uniform"):
-    """Stored-cost Problem from a point cloud (D1: dim 2, D3: dim 784 pixels)."""
+def pixel_cost_device(X, Y, device=None):
+    """The 8-bit point-set cost built on the GPU (K10, problems.py:87-111's
+    setup GEMM): ``max(|x|^2 + |y|^2 - 2 X Y^T, 0) / max`` from integer
+    intensities 0..255 (host arrays or CUDA tensors, n x d float64), computed
+    with exact u8 x u8 -> s32 tensor-core products, so the result equals the
+    host evaluation bit for bit (``otn_pixel_cost``).  Returns the n x n
+    float64 CUDA tensor (a view of the solver's ld-padded layout, reused by
+    the solver without a copy)."""
+    import torch
+
+    from ._device import Context, vptr
+    device = torch.device(device or "cuda")
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+
+    def dev(a):
+        t = a if torch.is_tensor(a) else torch.from_numpy(np.ascontiguousarray(a, np.float64))
+        return t.to(device=device, dtype=torch.float64).contiguous()
+    Xd, Yd = dev(X), dev(Y)
+    if Xd.ndim != 2 or Xd.shape != Yd.shape:
+        raise DimensionError(f"point sets must be n-by-d, got {tuple(Xd.shape)}, {tuple(Yd.shape)}")
+    n, d = int(Xd.shape[0]), int(Xd.shape[1])
+    ctx = Context.get(n, device)
+    buf = ctx.zeros((n, ctx.ld))
+    cmax = ctypes.c_double(0.0)
+    ctx.call("otn_pixel_cost", vptr(Xd), vptr(Yd), d, vptr(buf), ctypes.byref(cmax))
+    if not cmax.value > 0.0:
+        raise DomainError("pixel cost: all point pairs coincide (zero maximum)")
+    C = buf[:, :n]
+    C._otn_padded = buf                  # the solver's layout (DeviceCost uses it as is)
+    return C
+
+
+def dense_points_problem(n, dim, seed, kind="uniform", device=None):
+    """Stored-cost Problem from a point cloud (D1: dim 2, D3: dim 784 pixels).
+
+    device (pixel sets only): build C on that GPU (pixel_cost_device) instead
+    of on the host; the two are bit-identical."""
     pc = points_problem(n, dim, seed, kind)
+    if device is not None:
+        if kind != "pixel":
+            raise DomainError("device cost construction is for 8-bit pixel sets")
+        return Problem(C=pixel_cost_device(pc.X, pc.Y, device), r=pc.r, c=pc.c, label=pc.label)
     if dim <= 8:
         C = pc.materialize_cost()
     else:
@@ -270,12 +311,13 @@ def dense_points_problem(n, dim, seed, kind="uniform"):
     return Problem(C=C, r=pc.r, c=pc.c, label=pc.label)
 
 
-def workload(spec):
+def workload(spec, device=None):
     """Problem from a compact spec string (used by tests, bench and fixtures).
 
     ``grid:<side>:<l1|l2sq>:<seed>``  |  ``pts:<n>:<dim>:<seed>`` (uniform,
     stored C)  |  ``pix:<n>:<dim>:<seed>`` (8-bit points, stored C)  |
     ``otf:<n>:<dim>:<seed>`` (uniform points, on-the-fly PointCloudProblem).
+    device: build a ``pix`` cost on that GPU (pixel_cost_device).
     """
     kind, *rest = spec.split(":")
     if kind not in ("grid", "pts", "pix", "otf") or len(rest) != 3:
@@ -290,7 +332,7 @@ def workload(spec):
     if kind == "pts":
         return dense_points_problem(n, dim, seed, "uniform")
     if kind == "pix":
-        return dense_points_problem(n, dim, seed, "pixel")
+        return dense_points_problem(n, dim, seed, "pixel", device=device)
     if kind == "otf":
         return points_problem(n, dim, seed, "uniform")
     raise DomainError(f"unknown workload spec {spec!r}")
