@@ -179,6 +179,54 @@ __device__ void red_cnt_rel(const Buf& b, double* v, uint32_t& ep) {
   ep = e;
 }
 
+// variant 9/10: warp 0 alone does totals, arrive, wait, loads (9: lane 0 spins, the
+// other lanes wait at __syncwarp; 10: the whole warp polls the counter)
+template <bool WARP_POLL>
+__device__ void red_w0(const Buf& b, double* v, uint32_t& ep) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x;
+  for (int k = 0; k < 2; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0) for (int k = 0; k < 2; ++k) s_red[k][warp] = v[k];
+  __syncthreads();
+  const uint32_t e = ep + 1;
+  double* base = b.red + (e & 1) * 2 * STR;
+  if (warp == 0) {
+    for (int k = 0; k < 2; ++k) {
+      double t = warp_sum(lane < NW ? s_red[k][lane] : 0.0);
+      if (lane == 0) __stcg(base + k * STR + blockIdx.x, t);
+    }
+    __syncwarp();
+    const uint32_t target = e * uint32_t(G);
+    if (WARP_POLL) {
+      if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(b.cnt) : "memory");
+      while (true) {
+        const uint32_t c = ld_acq(b.cnt);
+        if (__all_sync(0xffffffffu, int32_t(c - target) >= 0)) break;
+      }
+    } else {
+      if (lane == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(b.cnt) : "memory");
+        while (int32_t(ld_acq(b.cnt) - target) < 0) {}
+      }
+      __syncwarp();
+    }
+    double2 p[2][4];
+    for (int k = 0; k < 2; ++k)
+      for (int m = 0; m < 4; ++m) {
+        int bb = 64 * m + 2 * lane;
+        p[k][m] = bb < G ? __ldcg(reinterpret_cast<const double2*>(base + k * STR + bb)) : make_double2(0, 0);
+      }
+    for (int k = 0; k < 2; ++k) {
+      double t = 0.0;
+      for (int m = 0; m < 4; ++m) t += p[k][m].x + p[k][m].y;
+      t = warp_sum(t);
+      if (lane == 0) s_res[k] = t;
+    }
+  }
+  __syncthreads();
+  v[0] = s_res[0]; v[1] = s_res[1];
+  ep = e;
+}
+
 // variant 4: arrival counter; the last arriver sums and broadcasts (value + epoch) in one line
 __device__ void red_last(const Buf& b, double* v, uint32_t& ep) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x;
@@ -250,6 +298,8 @@ __global__ void __launch_bounds__(NT, 1) k(Buf b, int variant, int reps) {
     else if (variant == 6) red_cnt_rel<true>(b, v, ep);
     else if (variant == 7) red_cnt_rel<false>(b, v, ep);
     else if (variant == 8) grid.sync();
+    else if (variant == 9) red_w0<false>(b, v, ep);
+    else if (variant == 10) red_w0<true>(b, v, ep);
     else red_last(b, v, ep);
     acc += v[0] + v[1];
   }
@@ -266,8 +316,9 @@ int main() {
   cudaMalloc(&b.out, 64);
   const char* names[] = {"cg grid.sync + loads", "flag poll", "flag poll + sleep 64", "counter + loads",
                          "counter, last arriver broadcasts", "flag poll + sleep 256",
-                         "counter (release red) + loads", "counter barrier only", "cg grid.sync only"};
-  for (int variant : {0, 8, 3, 6, 7, 4}) {
+                         "counter (release red) + loads", "counter barrier only", "cg grid.sync only",
+                         "warp 0: lane 0 spins", "warp 0: whole warp polls"};
+  for (int variant : {0, 3, 6, 7, 9, 10}) {
     for (int rep = 0; rep < 3; ++rep) {
       cudaMemset(b.gs, 0, 2 * 2 * STR * 16);
       cudaMemset(b.cnt, 0, 64);
