@@ -11,12 +11,13 @@ cp "$ROOT"/paper_2504_02067_b200/csrc/*.cu "$ROOT"/paper_2504_02067_b200/csrc/*.
    "$ROOT"/paper_2504_02067_b200/csrc/*.h "$tmp"/
 cp "$sub" "$tmp/$(basename "${3:-otn_cg.cu}")"
 cd "$tmp"
-for f in otn_lse otn_cg otn_vec otn_pc otn_capi; do
+srcs=$(ls *.cu | sed 's/\.cu$//')
+for f in $srcs; do
   nvcc -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -gencode arch=compute_100a,code=sm_100a \
        -c $f.cu -o $f.o &
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$ROOT/build/ab/libotn_$name.so" \
-     otn_lse.o otn_cg.o otn_vec.o otn_pc.o otn_capi.o -lcudart_static
+     $(for f in $srcs; do echo $f.o; done) -lcudart_static
 cd "$ROOT"; rm -rf "$tmp"
 echo "built build/ab/libotn_$name.so"
