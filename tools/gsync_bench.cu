@@ -227,6 +227,48 @@ __device__ void red_w0(const Buf& b, double* v, uint32_t& ep) {
   ep = e;
 }
 
+// variant 11/12: the arrival counter split over K lines (CTA b arrives on line
+// b % K, K lanes of warp 0 poll the K lines) + one read of the slots
+template <int K>
+__device__ void red_cntk(const Buf& b, double* v, uint32_t& ep) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x;
+  for (int k = 0; k < 2; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0) for (int k = 0; k < 2; ++k) s_red[k][warp] = v[k];
+  __syncthreads();
+  const uint32_t e = ep + 1;
+  double* base = b.red + (e & 1) * 2 * STR;
+  if (warp < 2) {
+    double t = warp_sum(lane < NW ? s_red[warp][lane] : 0.0);
+    if (lane == 0) base[warp * STR + blockIdx.x] = t;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(b.cnt + 32 * (blockIdx.x % K)) : "memory");
+    // line k receives the CTAs b = k mod K: ceil((G - k) / K) per exchange
+    const uint32_t per = lane < K ? uint32_t((G - lane + K - 1) / K) : 0u;
+    const uint32_t target = e * per;
+    while (true) {
+      const uint32_t c = lane < K ? ld_acq(b.cnt + 32 * lane) : 0u;
+      if (__all_sync(0xffffffffu, int32_t(c - target) >= 0)) break;
+    }
+  }
+  __syncthreads();
+  if (warp < 2) {
+    double t = 0.0;
+    for (int m = 0; m < STR / 64; ++m) {
+      int bb = 64 * m + 2 * lane;
+      double2 p = bb < G ? __ldcg(reinterpret_cast<const double2*>(base + warp * STR + bb)) : make_double2(0, 0);
+      t += p.x + p.y;
+    }
+    t = warp_sum(t);
+    if (lane == 0) s_res[warp] = t;
+  }
+  __syncthreads();
+  v[0] = s_res[0]; v[1] = s_res[1];
+  ep = e;
+}
+
 // variant 4: arrival counter; the last arriver sums and broadcasts (value + epoch) in one line
 __device__ void red_last(const Buf& b, double* v, uint32_t& ep) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x;
@@ -300,6 +342,9 @@ __global__ void __launch_bounds__(NT, 1) k(Buf b, int variant, int reps) {
     else if (variant == 8) grid.sync();
     else if (variant == 9) red_w0<false>(b, v, ep);
     else if (variant == 10) red_w0<true>(b, v, ep);
+    else if (variant == 11) red_cntk<4>(b, v, ep);
+    else if (variant == 12) red_cntk<8>(b, v, ep);
+    else if (variant == 13) red_cntk<16>(b, v, ep);
     else red_last(b, v, ep);
     acc += v[0] + v[1];
   }
@@ -312,16 +357,18 @@ int main() {
   Buf b;
   cudaMalloc(&b.red, 2 * 2 * STR * 8);
   cudaMalloc(&b.gs, 2 * 2 * STR * 16);
-  cudaMalloc(&b.cnt, 64);
+  cudaMalloc(&b.cnt, 32 * 4 * 16);
   cudaMalloc(&b.out, 64);
   const char* names[] = {"cg grid.sync + loads", "flag poll", "flag poll + sleep 64", "counter + loads",
                          "counter, last arriver broadcasts", "flag poll + sleep 256",
                          "counter (release red) + loads", "counter barrier only", "cg grid.sync only",
-                         "warp 0: lane 0 spins", "warp 0: whole warp polls"};
-  for (int variant : {0, 3, 6, 7, 9, 10}) {
+                         "warp 0: lane 0 spins", "warp 0: whole warp polls",
+                         "counter over 4 lines + loads", "counter over 8 lines + loads",
+                         "counter over 16 lines + loads"};
+  for (int variant : {3, 11, 12, 13}) {
     for (int rep = 0; rep < 3; ++rep) {
       cudaMemset(b.gs, 0, 2 * 2 * STR * 16);
-      cudaMemset(b.cnt, 0, 64);
+      cudaMemset(b.cnt, 0, 32 * 4 * 16);
       int reps = 2000;
       void* args[] = {&b, &variant, &reps};
       cudaEvent_t e0, e1;
