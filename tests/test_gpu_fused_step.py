@@ -15,11 +15,11 @@ from paper_2504_02067_b200.projector import ARMIJO_C1, ARMIJO_SLOPE_FLOOR
 pytestmark = pytest.mark.gpu
 
 
-def _state(spec="grid:16:l2sq:1", gamma=2.0 ** 8, seed=0, noise=0.05):
+def _state(spec="grid:16:l2sq:1", gamma=2.0 ** 8, seed=0):
     prob = problems.workload(spec)
     rng = np.random.default_rng(seed)
-    u = np.log(prob.r) + noise * rng.standard_normal(prob.n)
-    v = np.log(prob.c) + noise * rng.standard_normal(prob.n)
+    u = np.log(prob.r) + 0.05 * rng.standard_normal(prob.n)
+    v = np.log(prob.c) + 0.05 * rng.standard_normal(prob.n)
     st = DualState(prob, gamma, u=u, v=v)
     st.rebalance_columns()
     return prob, st
@@ -181,42 +181,3 @@ def test_persistent_launch_timing():
     assert k.coop_timing() is False
     with pytest.raises(OTNError):
         k.coop_ms()
-
-
-@pytest.mark.parametrize("spec,gamma", [("grid:16:l2sq:1", 2.0 ** 4), ("pix:256:784:0", 2.0 ** 4)])
-def test_system_ahead_matches_a_fresh_system(spec, gamma):
-    """otn_system_ahead (the next step's system, built on the device behind
-    the step and gated by the projector's continue test) equals the system
-    the host would build after the step; with the gate closed (the gradient
-    already below eps_d) it leaves the system buffers untouched."""
-    _, a = _state(spec, gamma, noise=0.002)
-    _, b = _state(spec, gamma, noise=0.002)
-    eta = 0.5
-    for st in (a, b):
-        st._row_grad_norm()
-    sa, sb = a._system(), b._system()
-    (da, dva), (db, dvb) = a._dir_bufs(), b._dir_bufs()
-    before = [t.clone() for t in (*a._sysbufs, a._plan_buf[0], a._plan_buf[1])]
-    # closed gate: eps_d above any gradient norm
-    res, mass, rowstat = _newton_step_device(a, sa, a._g, eta, 0.0, False, None, da, dva,
-                                             ARMIJO_C1, ARMIJO_SLOPE_FLOOR, ahead=(1e300, 1.0))
-    assert rowstat is not None, "step not accepted; pick another case"
-    after = [t for t in (*a._sysbufs, a._plan_buf[0], a._plan_buf[1])]
-    for x, y in zip(before, after):
-        assert bool((x == y).all())
-    # open gate: a fresh state, the same step, then compare with b's host-built system
-    _, a = _state(spec, gamma, noise=0.002)
-    a._row_grad_norm()
-    sa = a._system()
-    da, dva = a._dir_bufs()
-    res_a, _, rowstat_a = _newton_step_device(a, sa, a._g, eta, 0.0, False, None, da, dva,
-                                              ARMIJO_C1, ARMIJO_SLOPE_FLOOR, ahead=(1e-300, 1e300))
-    res_b, _, rowstat_b = _newton_step_device(b, sb, b._g, eta, 0.0, False, None, db, dvb,
-                                              ARMIJO_C1, ARMIJO_SLOPE_FLOOR)
-    assert rowstat_a == rowstat_b and rowstat_a is not None
-    a._cache_valid = b._cache_valid = True
-    pre = a._system_prebuilt()
-    fresh = b._system()
-    for x, y in ((pre._P, fresh._P), (pre._rP, fresh._rP), (pre._cP, fresh._cP),
-                 (pre._icP, fresh._icP), (pre._mu(), fresh._mu()), (pre._mask, fresh._mask)):
-        assert bool((x == y).all())
