@@ -270,17 +270,6 @@ int otn_newton_step(otn_ctx* ctx, const double* P, const uint64_t* seg_mask, con
  * host_res / host_out / host_flags as otn_newton_step would have.           */
 int otn_newton_step_wait(otn_ctx* ctx, otn_solve_result* host_res, double* host_out,
                          int* host_flags);
-/* The next Newton step's system (otn_system_prep into rP, cP, icP + the
- * otn_materialize of P, mu, seg_mask) enqueued behind an otn_newton_step
- * (before its _wait), run on the device iff that step's trial was accepted
- * and its row statistics send the projector straight into another Newton
- * step: ||grad||_1 > eps_d, no statistics flag, (sum - 1) <= eps_chi
- * (projector.py:152-260's loop; the host takes the same decision from the
- * same values after the wait and then uses the buffers as built).         */
-int otn_system_ahead(otn_ctx* ctx, const double* lr, const double* lc, double* rP, double* cP,
-                     double* icP, const double* C, double neg_gamma, const double* u,
-                     const double* v, double* P, double* mu, uint64_t* seg_mask, double eps_d,
-                     double eps_chi);
 
 /* Telemetry: with timing on, every persistent-solver launch (the partition
  * kernel + k_coop) is bracketed by CUDA events; otn_coop_ms waits for the

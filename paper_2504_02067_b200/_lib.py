@@ -103,7 +103,6 @@ SIGNATURES = {
     "otn_newton_step": [_P, _P, _P, _P, _P, _P, _P, _D, _D, _I, _I64, _P, _P, _P, _P, _I, _D, _P, _P,
                         _P, _P, _P, _P, _P, _P, _D, _D, ctypes.POINTER(SolveResult), _DP, _IP],
     "otn_newton_step_wait": [_P, ctypes.POINTER(SolveResult), _DP, _IP],
-    "otn_system_ahead": [_P, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P, _P, _P, _D, _D],
     "otn_probe": [_P, _P, _P, _P, _P, _P, _P, _I, _I64],
     "otn_coop_layout": [_P],
     "otn_pc_pass": [_P, _I, _P, _I64, _I64, _P, _I64, _I64, _I, _D, _D, _I, _P, _P, _D, _P, _P,

@@ -463,21 +463,6 @@ int otn_system_prep(otn_ctx* x, const double* lr, const double* lc, double* rP, 
   return OTN_OK;
 }
 
-int otn_system_ahead(otn_ctx* x, const double* lr, const double* lc, double* rP, double* cP,
-                     double* icP, const double* C, double ng, const double* u, const double* v,
-                     double* P, double* mu, uint64_t* seg_mask, double eps_d, double eps_chi) {
-  DeviceGuard dg_(x);
-  OTN_REQUIRE(x && lr && lc && rP && cP && icP && C && u && v && P && mu,
-              "otn_system_ahead: NULL argument");
-  int* gate = x->flags + 13;
-  OTN_CUDA(otn::launch_ahead_gate(x, eps_d, eps_chi, gate), "otn_system_ahead: gate");
-  OTN_CUDA(otn::launch_sys_prep(x, lr, lc, rP, cP, icP, x->flags + 1, gate),
-           "otn_system_ahead: prep");
-  OTN_CUDA(otn::launch_materialize(x, C, ng, u, v, P, icP, rP, mu, x->flags + 0, seg_mask, gate),
-           "otn_system_ahead: plan");
-  return OTN_OK;
-}
-
 int otn_square_matvec(otn_ctx* x, const double* P, const double* w, double* out) {
   DeviceGuard dg_(x);
   OTN_REQUIRE(x && P && w && out, "otn_square_matvec: NULL argument");

@@ -82,12 +82,10 @@ cudaError_t launch_lse_cols(otn_ctx* x, const double* C, double ng, const double
                             double alpha, int mode, double* out, const int* gate = nullptr);
 cudaError_t launch_materialize(otn_ctx* x, const double* C, double ng, const double* u,
                                const double* v, double* P, const double* icP, const double* rP,
-                               double* mu, int* flag, uint64_t* mask, const int* gate = nullptr);
+                               double* mu, int* flag, uint64_t* mask);
 cudaError_t launch_plan_mask(otn_ctx* x, const double* P, uint64_t* mask);
 cudaError_t launch_sys_prep(otn_ctx* x, const double* log_rP, const double* log_cP, double* rP,
-                            double* cP, double* icP, int* flag, const int* gate = nullptr);
-// otn_system_ahead's gate (see k_ahead_gate): writes *gate
-cudaError_t launch_ahead_gate(otn_ctx* x, double eps_d, double eps_chi, int* gate);
+                            double* cP, double* icP, int* flag);
 cudaError_t launch_square_matvec(otn_ctx* x, const double* P, const double* w, double* out);
 
 // Persistent cooperative solver.

@@ -401,11 +401,9 @@ template <bool FULL>
 __global__ void __launch_bounds__(kMatThreads) k_materialize(const double* __restrict__ C,
     int64_t n, int64_t ld, double ng, const double* __restrict__ u, const double* __restrict__ v,
     double* __restrict__ P, const double* __restrict__ icP, const double* __restrict__ rP,
-    double* __restrict__ mu, int* __restrict__ flag, uint64_t* __restrict__ mask,
-    const int* __restrict__ gate) {
+    double* __restrict__ mu, int* __restrict__ flag, uint64_t* __restrict__ mask) {
   __shared__ double2 s_exp[64];
   __shared__ double s_v[2][256], s_ic[2][256];
-  if (gate && *gate == 0) return;                   // uniform over the grid
   exp_tab_load(s_exp);
   const int64_t row = int64_t(blockIdx.x) * (kMatThreads / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -525,9 +523,9 @@ __global__ void __launch_bounds__(kLseThreads) k_plan_mask(const double* __restr
 }
 
 __global__ void k_sys_prep(int64_t n, const double* __restrict__ lr, const double* __restrict__ lc,
-                           double* rP, double* cP, double* icP, int* flag, const int* gate) {
+                           double* rP, double* cP, double* icP, int* flag) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n || (gate && *gate == 0)) return;
+  if (i >= n) return;
   const double rp = exp_fast(lr[i]), cp = exp_fast(lc[i]);
   rP[i] = rp;
   cP[i] = cp;
@@ -551,25 +549,6 @@ __global__ void __launch_bounds__(kLseThreads) k_square_matvec(const double* __r
   }
   acc = warp_sum(acc);
   if (lane == 0) out[row] = acc;
-}
-
-// The gate of a speculatively enqueued next system (otn_system_ahead): the
-// step's trial was accepted and its row statistics send the projector straight
-// to another Newton step (projector.py: ||grad||_1 > eps_d, no chi-square
-// sweep, clean statistics).  Resets the system's flags when it opens.
-__global__ void k_ahead_gate(const int* accepted, const double* stats, const int* stat_flags,
-                             double eps_d, double eps_chi, int* gate, int* sys_flags) {
-  const double l1 = stats[0], s = stats[1];
-  const int open = *accepted != 0 && l1 > eps_d && *stat_flags == 0 &&
-                   !(__dsub_rn(s, 1.0) > eps_chi);
-  *gate = open;
-  if (open) { sys_flags[0] = 0; sys_flags[1] = 0; }
-}
-
-cudaError_t launch_ahead_gate(otn_ctx* x, double eps_d, double eps_chi, int* gate) {
-  k_ahead_gate<<<1, 1, 0, x->stream>>>(x->flags + 7, x->scal + 33, x->flags + 8, eps_d, eps_chi,
-                                       gate, x->flags);
-  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -613,14 +592,14 @@ cudaError_t launch_lse_cols(otn_ctx* x, const double* C, double ng, const double
 
 cudaError_t launch_materialize(otn_ctx* x, const double* C, double ng, const double* u,
                                const double* v, double* P, const double* icP, const double* rP,
-                               double* mu, int* flag, uint64_t* mask, const int* gate) {
+                               double* mu, int* flag, uint64_t* mask) {
   const unsigned grid = rows_grid(x->n, kMatThreads);
   if (x->n == x->ld && x->n % 256 == 0)
     k_materialize<true><<<grid, kMatThreads, 0, x->stream>>>(C, x->n, x->ld, ng, u, v, P, icP, rP,
-                                                             mu, flag, mask, gate);
+                                                             mu, flag, mask);
   else
     k_materialize<false><<<grid, kMatThreads, 0, x->stream>>>(C, x->n, x->ld, ng, u, v, P, icP, rP,
-                                                              mu, flag, mask, gate);
+                                                              mu, flag, mask);
   return cudaGetLastError();
 }
 
@@ -630,9 +609,8 @@ cudaError_t launch_plan_mask(otn_ctx* x, const double* P, uint64_t* mask) {
 }
 
 cudaError_t launch_sys_prep(otn_ctx* x, const double* lr, const double* lc, double* rP,
-                            double* cP, double* icP, int* flag, const int* gate) {
-  k_sys_prep<<<unsigned((x->n + 255) / 256), 256, 0, x->stream>>>(x->n, lr, lc, rP, cP, icP, flag,
-                                                                  gate);
+                            double* cP, double* icP, int* flag) {
+  k_sys_prep<<<unsigned((x->n + 255) / 256), 256, 0, x->stream>>>(x->n, lr, lc, rP, cP, icP, flag);
   return cudaGetLastError();
 }
 

@@ -345,7 +345,7 @@ class DualState:
         self._touch_KT()
 
     def _newton_step(self, sys, eta, rho0, zero_init, max_cg_iters, d_u, d_v, armijo_c1,
-                     slope_floor, ahead=None):
+                     slope_floor):
         """Newton direction + first trial + (if accepted) accept path in one
         synchronization (otn_newton_step); see projector.project."""
         from .newton import _newton_step_device
@@ -354,7 +354,7 @@ class DualState:
         prework = self.__dict__.pop("_prework", None)
         res, mass, rowstat = _newton_step_device(self, sys, self._g, eta, rho0, zero_init,
                                                  max_cg_iters, d_u, d_v, armijo_c1, slope_floor,
-                                                 prework=prework, ahead=ahead)
+                                                 prework=prework)
         if rowstat is not None:
             # the device ran _accept(1.0, d_u, d_v) + refresh_rows_only + _row_stats
             self._cache_valid = True
@@ -442,16 +442,6 @@ class DualState:
     def _system(self):
         from .newton import DiscountedSystem
         return DiscountedSystem.from_state(self, check_flags=False)   # the Newton launch checks
-
-    def _system_prebuilt(self):
-        """The system otn_system_ahead built on the device behind the last
-        Newton step (the buffers and tallies of _system, nothing enqueued)."""
-        from .newton import DiscountedSystem
-        rP, cP, icP, mu = self._sysbufs
-        opcount.add(4)                              # materialize_plan, as in _materialize
-        self._touch_K()
-        P, mask = self._plan_buf
-        return DiscountedSystem(P, rP, cP, _ctx=self._ctx, _mu=mu, _icP=icP, _mask=mask)
 
     def _dir_bufs(self):
         bufs = getattr(self, "_dirbufs", None)

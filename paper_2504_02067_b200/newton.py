@@ -262,7 +262,7 @@ def _newton_device(grad_u, sys, eta, rho0, zero_init, max_cg_iters, d_u, d_v):
 
 
 def _newton_step_device(state, sys, grad_u, eta, rho0, zero_init, max_cg_iters, d_u, d_v,
-                        armijo_c1, slope_floor, prework=None, ahead=None):
+                        armijo_c1, slope_floor, prework=None):
     """One otn_newton_step launch sequence for a DualState: the Newton
     direction, its trial at alpha = 1 and, when the Armijo test passes there,
     the accept path, with one host synchronization.  Returns
@@ -289,17 +289,7 @@ def _newton_step_device(state, sys, grad_u, eta, rho0, zero_init, max_cg_iters, 
                 vptr(state._trial_vec), vptr(state._lc), vptr(state._lr), vptr(state._g))
         cached = state._nstep_ptrs = (key, head, mid, tail)
     _, head, mid, tail = cached
-    ahead_args = None
-    if ahead is not None:
-        # the next step's system, built behind this step on the device iff
-        # the projector will go straight into another Newton step
-        bufs, plan = getattr(state, "_sysbufs", None), getattr(state, "_plan_buf", None)
-        if bufs is not None and plan is not None:
-            rP, cP, icP, mu = bufs
-            ahead_args = (vptr(state._lr), vptr(state._lc), vptr(rP), vptr(cP), vptr(icP),
-                          state._dc.ptr(), state._ng, vptr(state._u), vptr(state._v),
-                          vptr(plan[0]), vptr(mu), vptr(plan[1]), float(ahead[0]), float(ahead[1]))
-    if prework is None and ahead_args is None:
+    if prework is None:
         k.call("otn_newton_step", *head, float(eta), float(rho0), int(bool(zero_init)),
                int(max_cg_iters), *mid, state._ng, *tail,
                float(armijo_c1), float(slope_floor), ctypes.byref(res), out, ctypes.byref(fl))
@@ -308,10 +298,7 @@ def _newton_step_device(state, sys, grad_u, eta, rho0, zero_init, max_cg_iters, 
         k.call("otn_newton_step", *head, float(eta), float(rho0), int(bool(zero_init)),
                int(max_cg_iters), *mid, state._ng, *tail,
                float(armijo_c1), float(slope_floor), None, None, None)
-        if ahead_args is not None:
-            k.call("otn_system_ahead", *ahead_args)
-        if prework is not None:
-            prework()
+        prework()
         k.call("otn_newton_step_wait", ctypes.byref(res), out, ctypes.byref(fl))
     if timed:
         TELEMETRY.coop.append((k.coop_ms(), int(res.hvps), 1, k.n, int(res.plan_mode),
