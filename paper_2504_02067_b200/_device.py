@@ -61,7 +61,7 @@ LAUNCHES = {
     "otn_newton_step": 9, "otn_newton_step_wait": 0,
     "otn_vec": 1, "otn_reduce": 1, "otn_row_stats": 1, "otn_accept": 1, "otn_reduce_async": 1, "otn_round_plan": 10, "otn_pc_pass": 1,
     "otn_vec_n": 1, "otn_reduce_n": 1, "otn_reduce_dev": 1, "otn_zero": 0,
-    "otn_is_symmetric": 1, "otn_transpose": 1,
+    "otn_is_symmetric": 1, "otn_transpose": 1, "otn_pixel_cost": 3,
 }
 
 
