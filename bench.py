@@ -456,7 +456,7 @@ def d3_from_points(dev, gi, gf, host_C):
     return {"from_points_e2e_s": time.perf_counter() - t0, "cost_build_s": t_cost,
             "from_points_solve_s": t_solve, "cost_bitwise_equal_host": same,
             "from_points_h2d_bytes": 2 * X.nbytes, "from_points_d2h_bytes": Ph.numel() * 8,
-            "cost_build": "otn_pixel_cost: u8 x u8 -> s32 mma.sync (exact), "
+            "cost_build": "otn_pixel_cost: u8 x u8 -> s32 tcgen05.mma kind::i8 (exact), "
                           "then /max; host numpy builds the same C in ~0.2 s"}
 
 
