@@ -240,7 +240,10 @@ def _sparse_plan(n, per_row, seed, heavy=0):
 @pytest.mark.parametrize("n,per_row,heavy,mode", [
     (64, 3, 0, 2), (300, 8, 0, 2), (1024, 20, 5, 2), (4096, 12, 9, 2),
     (1024, 1024, 0, 0), (4096, 600, 0, 3), (2048, 1400, 0, 0), (2048, 2048, 0, 0),
-    (4096, 4096, 0, 0)])
+    (4096, 4096, 0, 0),
+    # wider than one 4096-column tile (ld 6016, 9024): the streamed ring over
+    # several tiles and the multi-slice column pass (ld > 32 x 148)
+    (6000, 6000, 0, 0), (9000, 60, 0, 0)])
 def test_hvp_plan_modes(n, per_row, heavy, mode):
     """Every plan mode (0 streamed ring, 2 sparse shared-memory rows, 3 sparse
     global-memory rows; mode 1 is retired) against numpy on the same plan; the
@@ -341,3 +344,24 @@ print("bulk ok")
     out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
                          env=dict(os.environ, OTN_LSE_BULK="1"), timeout=600)
     assert out.returncode == 0 and "bulk ok" in out.stdout, out.stderr[-3000:]
+
+
+def test_wide_mdot_matches_oracle():
+    """A full mdot on a cost wider than one tile (n = 5184 > 4096: several
+    column tiles, the multi-slice column pass, residual replacement there)
+    against the oracle restatement of the reference, same seeded problem."""
+    spec, gi, gf = "grid:72:l2sq:0", 2.0 ** 5, 2.0 ** 8
+    prob = problems.workload(spec)
+    import os
+    orc.set_threads(os.cpu_count() or 1)               # bit-identical for any thread count
+    run = orc.mdot(prob.C, prob.r, prob.c, gi, gf)
+    import torch
+    from paper_2504_02067_b200 import mdot
+    dp = problems.Problem(C=torch.from_numpy(prob.C).cuda(), r=prob.r, c=prob.c)
+    sol = mdot(dp, gi, gf)
+    got = [(it.gamma, it.stats.newton_steps, it.stats.cg_iters) for it in sol.iterations]
+    want = [(g, pr.newton_steps, pr.cg_iters) for (_t, g, _eps, _q, pr) in run.stages]
+    assert got == want
+    du = np.abs(sol.final_state.u - run.state.u).max() / np.abs(run.state.u).max()
+    dv = np.abs(sol.final_state.v - run.state.v).max() / np.abs(run.state.v).max()
+    assert du <= 1e-10 and dv <= 1e-10, (du, dv)
