@@ -7,12 +7,13 @@ Gates:
             stage count, identical per-stage Newton-step and CG-iteration counts,
             identical op tallies, u and v within max(1e-10, SPREAD_X x the
             reference's own spread) (inf-norm relative);
-  spread  — squared-L2 grids and the 784-d pixel sets, where the reference
-            does not reproduce itself to 1e-9 (D2-L2^2: 789 vs
-            785 CG in stage 14, u within 3.4e-11): identical gamma schedule and
-            Newton counts, each stage's CG count within the reference's own
-            det-vs-BLAS difference for that stage (so equal wherever the
-            reference agrees with itself), u and v within max(1e-10, SPREAD_X x
+  spread  — where the reference does not reproduce itself to 1e-9, and the
+            order-sensitive D2-L2^2 class (seed 0:
+            789 vs 785 CG in stage 14, u within 3.4e-11): identical gamma
+            schedule and Newton counts, each stage's CG count within that stage's
+            det-vs-BLAS difference or, for the D2-L2^2 class, within the class's
+            largest relative det-vs-BLAS difference (per stage and in total, over
+            every seed of the class), u and v within max(1e-10, SPREAD_X x
             its self-spread),
             primal within 1e-9 relative, true-marginal error <= 1e-6 at full size.
 """
@@ -32,12 +33,43 @@ pytestmark = pytest.mark.gpu
 # are logged per case (profiles/r02_parity_gates.txt) -- most are below 10.
 SPREAD_X = 100
 
+# Configuration classes whose CG counts move under any change of summation
+# order (SURVEY.md §6 "Measured noise floor": the n = 4096 squared-L2 grid --
+# the reference's own reorderings differ by up to 4 CG in a stage at n = 4096
+# and 7 at n = 1024, even where a given seed's two runs happen to agree).
+# Their goldens are held to the spread gate, with the class's spread: the
+# largest relative BLAS-vs-deterministic difference the reference shows on any
+# seed of the class (per stage and in total).
+ORDER_SENSITIVE = ("grid:64:l2sq",)
+
+
+def config_class(meta):
+    return meta["spec"].rsplit(":", 1)[0]
+
+
+def class_spread(cls):
+    """(per-stage, total) relative CG spread of the reference over every golden
+    of the class: max |det - BLAS| / BLAS."""
+    rel_stage, rel_total = 0.0, 0.0
+    for name in traj_names():
+        meta, _ = load_traj(name)
+        ss = meta.get("self_spread")
+        if config_class(meta) != cls or ss is None:
+            continue
+        ref = [s["cg_iters"] for s in meta["stages"]]
+        for a, b in zip(ss["cg"], ref):
+            rel_stage = max(rel_stage, abs(a - b) / max(b, 1))
+        rel_total = max(rel_total, abs(ss["cg_total"] - sum(ref)) / max(sum(ref), 1))
+    return rel_stage, rel_total
+
+
 def gate(meta):
-    """strict iff the reference is reproducible against itself on this case:
-    BLAS vs OTN_DETERMINISTIC=1 give identical per-stage counts and potentials
-    within 1e-9 (recorded by make_golden.py as meta['self_spread'])."""
+    """strict iff the reference is reproducible against itself on this case
+    (BLAS vs OTN_DETERMINISTIC=1 give identical per-stage counts and potentials
+    within 1e-9, meta['self_spread']) and the configuration is not an
+    order-sensitive class."""
     ss = meta.get("self_spread")
-    if ss is None:
+    if ss is None or config_class(meta) in ORDER_SENSITIVE:
         return "spread"
     same = (ss["stages"] == len(meta["stages"])
             and ss["cg"] == [s["cg_iters"] for s in meta["stages"]]
@@ -118,10 +150,14 @@ def check(meta, arr, sol, name):
         assert [it.gamma for it in sol.iterations] == [s["gamma"] for s in meta["stages"]]
         assert got_newton == ref_newton, (got_newton, ref_newton)
         det_cg = ss["cg"]
+        rel_stage, rel_total = (class_spread(config_class(meta))
+                                if config_class(meta) in ORDER_SENSITIVE else (0.0, 0.0))
         for k, (a, b, c) in enumerate(zip(got_cg, ref_cg, det_cg)):
-            assert abs(a - b) <= abs(c - b), ("stage", k, a, b, c)
-        assert abs(sum(got_cg) - sum(ref_cg)) <= abs(ss["cg_total"] - sum(ref_cg)), \
-            (sum(got_cg), sum(ref_cg), ss["cg_total"])
+            tol_k = max(abs(c - b), int(np.ceil(rel_stage * b)))
+            assert abs(a - b) <= tol_k, ("stage", k, a, b, c, tol_k)
+        tol_t = max(abs(ss["cg_total"] - sum(ref_cg)), int(np.ceil(rel_total * sum(ref_cg))))
+        assert abs(sum(got_cg) - sum(ref_cg)) <= tol_t, (sum(got_cg), sum(ref_cg), ss["cg_total"],
+                                                          tol_t)
         tol = max(1e-10, SPREAD_X * ss["du"], SPREAD_X * ss["dv"])
         assert du <= tol and dv <= tol, (du, dv, tol)
         assert sol.primal_cost == pytest.approx(meta["primal"], rel=1e-9, abs=1e-14)
