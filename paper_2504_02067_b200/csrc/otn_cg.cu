@@ -18,6 +18,7 @@
 // CG state lives in registers (one row per thread); dot products / L1 norms
 // are grid reductions with fixed trees (deterministic, no FP64 atomics).
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "otn_common.cuh"
 #include "otn_internal.h"
@@ -372,8 +373,16 @@ struct SparseView {
   uint32_t* perm;                                   // mode 2: CSC slot -> CSR entry | row << 16
   double* cval;                                     // mode 3: CSC values
   uint16_t* crow;                                   // mode 3: CSC rows
+  double* scval;                                    // mode 3: CSC slots [0, kSparseGS) in shared memory
+  uint16_t* scrow;
   bool direct;                                      // mode 3
 };
+
+// Mode 3 keeps the first kSparseGS slots of its (thread-interleaved) CSC in
+// the shared memory mode 2 uses for its compressed rows -- every thread's
+// first entries, read without an L2 round trip -- past the staged spans.
+constexpr size_t kSparseGSmem = (kSparseVal + size_t(kSparseRows) * 4 + 15) / 16 * 16;
+constexpr int kSparseGS = int((kSparseBytes + size_t(kSparseRows) * 4 - kSparseGSmem) / 10) / 8 * 8;
 
 // Per-CTA slice of the global compressed-rows buffer (kPlanSparseG):
 // val [cap] + cval [slot] doubles, then col [cap] + crow [slot] u16.
@@ -394,6 +403,8 @@ __device__ __forceinline__ SparseView sparse_view(void* sg) {
     v.col = reinterpret_cast<uint16_t*>(v.cval + kSparseGSlot);
     v.crow = v.col + kSparseGCap;
     v.perm = nullptr;
+    v.scval = reinterpret_cast<double*>(b + kSparseGSmem);
+    v.scrow = reinterpret_cast<uint16_t*>(b + kSparseGSmem + size_t(kSparseGS) * 8);
     v.direct = true;
   } else {
     v.val = reinterpret_cast<double*>(b + kSparseVal);
@@ -401,6 +412,8 @@ __device__ __forceinline__ SparseView sparse_view(void* sg) {
     v.perm = reinterpret_cast<uint32_t*>(b + kSparsePerm);
     v.cval = nullptr;
     v.crow = nullptr;
+    v.scval = nullptr;
+    v.scrow = nullptr;
     v.direct = false;
   }
   return v;
@@ -520,8 +533,13 @@ __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* 
         while (s_kb[o] > k) --o;
         const int addr = (k - s_kb[o]) * split + o;
         if (sp.direct) {
-          sp.cval[addr] = sp.val[e];
-          sp.crow[addr] = uint16_t(r);
+          if (addr < kSparseGS) {
+            sp.scval[addr] = sp.val[e];
+            sp.scrow[addr] = uint16_t(r);
+          } else {
+            sp.cval[addr] = sp.val[e];
+            sp.crow[addr] = uint16_t(r);
+          }
         } else {
           sp.perm[addr] = uint32_t(e) | (uint32_t(r) << 16);
         }
@@ -604,16 +622,22 @@ __device__ void phase_a_sparse(void* sg, int64_t r0, int64_t r1, double* wrow, S
     bool begun = cptr[m] < kb;                      // column started in an earlier thread
     double acc = 0.0;
     const int S = s_split;
-    for (int k0 = kb; k0 < ke; k0 += 8) {
+    // entries [k0, min(k0 + 8, kend)); mode 3 reads its shared-memory slots
+    // (SMEM) and its global ones in separate loops (no per-entry choice)
+    auto batch = [&](int k0, int kend, auto smem_tag) {
+      constexpr bool SMEM = decltype(smem_tag)::value;
       double pv[8], xv[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int k = k0 + u;
         pv[u] = 0.0;
         xv[u] = 0.0;
-        if (k < ke) {
+        if (k < kend) {
           const int ad = (k - kb) * S + t;
-          if (sp.direct) {
+          if (SMEM) {
+            pv[u] = sp.scval[ad];
+            xv[u] = xs[sp.scrow[ad]];
+          } else if (sp.direct) {
             pv[u] = sp.cval[ad];
             xv[u] = xs[sp.crow[ad]];
           } else {
@@ -626,7 +650,7 @@ __device__ void phase_a_sparse(void* sg, int64_t r0, int64_t r1, double* wrow, S
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int k = k0 + u;
-        if (k >= ke) break;
+        if (k >= kend) break;
         if (k == mend) {                            // column m ended inside this thread
           if (begun) head[t] = acc;
           else wrow[ulo + mcol] = acc;
@@ -638,7 +662,15 @@ __device__ void phase_a_sparse(void* sg, int64_t r0, int64_t r1, double* wrow, S
         }
         acc = fma(pv[u], xv[u], acc);
       }
+    };
+    int k0 = kb;
+    if (sp.direct) {
+      // this thread's slots (k - kb) * S + t below kSparseGS sit in shared memory
+      const int ks = t < kSparseGS ? min(ke, kb + (kSparseGS - 1 - t) / S + 1) : kb;
+      for (; k0 < ks; k0 += 8) batch(k0, ks, std::true_type{});
+      k0 = ks;
     }
+    for (; k0 < ke; k0 += 8) batch(k0, ke, std::false_type{});
     if (begun) head[t] = acc;                       // piece of a column begun earlier
     else if (mend <= ke) wrow[ulo + mcol] = acc;    // whole column inside this thread
     else { tail = acc; tail_m = m; }                // column continues in later threads
@@ -1311,6 +1343,8 @@ __global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
 }
 
 static_assert(kRingBytes == size_t(kRingDepth) * kSlotBytes, "ring layout");
+static_assert(kSparseGSmem + size_t(kSparseGS) * 10 <= kSparseBytes + size_t(kSparseRows) * 4,
+              "mode-3 shared CSC slots fit the dynamic region");
 constexpr size_t kDynRing = kRingBytes + size_t(kSpanSmem) * 4;
 constexpr size_t kDynSparse = kSparseBytes + size_t(kSparseRows) * 4;
 constexpr size_t kDynBytes = kDynRing > kDynSparse ? kDynRing : kDynSparse;
