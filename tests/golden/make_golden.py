@@ -65,6 +65,17 @@ SINKHORN = [
     ("sk_pts1024_3d_s0", "pts:1024:3:0", 2.0 ** 5, 2.0 ** 9),
 ]
 
+# ragged, mid-size cases (n = 1000 ... 3000, not a multiple of the 32-column
+# padding or of the CTA counts); oracle-verified, GPU-checked, not re-run by
+# the CPU suite (names start with "M")
+MEDIUM = [
+    ("M_grid45_l2sq_s2", "grid:45:l2sq:2", 2.0 ** 5, 2.0 ** 13),
+    ("M_grid40_l1_s4", "grid:40:l1:4", 2.0 ** 5, 2.0 ** 12),
+    ("M_pts2000_3d_s1", "pts:2000:3:1", 2.0 ** 5, 2.0 ** 11),
+    ("M_pix1000_784_s1", "pix:1000:784:1", 2.0 ** 5, 2.0 ** 12),
+    ("M_pts3000_2d_s2", "pts:3000:2:2", 2.0 ** 5, 2.0 ** 12),
+]
+
 LARGE = [
     ("D2_grid64_l1_s0", "grid:64:l1:0", 2.0 ** 5, 2.0 ** 16),
     ("D2_grid64_l2sq_s0", "grid:64:l2sq:0", 2.0 ** 5, 2.0 ** 16),
@@ -241,6 +252,7 @@ def kernel_goldens():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--large", action="store_true", help="also the n=4096 D2/D3 cases")
+    ap.add_argument("--medium", action="store_true", help="also the ragged mid-size cases")
     ap.add_argument("--only", default=None)
     ap.add_argument("--verify-oracle", action="store_true")
     args = ap.parse_args()
@@ -248,6 +260,7 @@ def main():
     orc.set_threads(os.cpu_count())       # slab-parallel oracle: bit-identical results
     kernel_goldens()
     cases = ([c + ("newton",) for c in SMALL] + [c + ("sinkhorn",) for c in SINKHORN]
+             + ([c + ("newton",) for c in MEDIUM] if args.medium else [])
              + ([c + ("newton",) for c in LARGE] if args.large else []))
     for name, spec, gi, gf, projector in cases:
         if args.only and args.only not in name:

@@ -15,7 +15,7 @@ from conftest import load_traj, traj_names
 from oracle import otn_oracle as orc
 from paper_2504_02067_b200 import problems
 
-FAST = [n for n in traj_names() if not n.startswith("D")]
+FAST = [n for n in traj_names() if not n.startswith(("D", "M"))]   # (M, D: GPU-checked only)
 
 
 def _trajectory(run):
