@@ -83,6 +83,8 @@ LARGE = [
     ("D2_grid64_l2sq_s2", "grid:64:l2sq:2", 2.0 ** 5, 2.0 ** 16),
     ("D2_grid64_l2sq_s3", "grid:64:l2sq:3", 2.0 ** 5, 2.0 ** 16),
     ("D3_pix4096_784_s0", "pix:4096:784:0", 2.0 ** 5, 2.0 ** 16),
+    ("D2_grid64_l1_s1", "grid:64:l1:1", 2.0 ** 5, 2.0 ** 16),
+    ("D3_pix4096_784_s1", "pix:4096:784:1", 2.0 ** 5, 2.0 ** 16),
 ]
 
 
