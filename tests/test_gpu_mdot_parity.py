@@ -233,3 +233,31 @@ def test_fused_newton_step_matches_per_call_path(spec, monkeypatch):
     sb = [(it.stats.newton_steps, it.stats.cg_iters, it.stats.backtracks) for it in b.iterations]
     assert sa == sb
     print(spec, "backtracks", sum(x[2] for x in sa), "steps", sum(x[0] for x in sa))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 33])
+def test_tiny_problems_match_oracle(n):
+    """Edge sizes against the oracle restatement of the reference: n = 1 fails
+    the same way (a zero-entropy marginal makes eps_d 0: DomainError), n = 2,
+    3, 5, 33 give the same stage-by-stage CG counts and potentials."""
+    from oracle import otn_oracle as orc
+    from paper_2504_02067_b200.errors import DomainError
+    rng = np.random.default_rng(n)
+    C = rng.random((n, n))
+    C = C / C.max() if n > 1 else np.zeros((1, 1))
+    r = np.full(n, 1.0 / n)
+    c = rng.random(n) + 0.5
+    c /= c.sum()
+    prob = problems.Problem(C=C, r=r, c=c)
+    if n == 1:
+        with pytest.raises(DomainError):
+            mdot(prob, 2.0 ** 2, 2.0 ** 8)
+        with pytest.raises(orc.OracleFailure):
+            orc.mdot(C, r, c, 2.0 ** 2, 2.0 ** 8)
+        return
+    sol = mdot(prob, 2.0 ** 2, 2.0 ** 8)
+    run = orc.mdot(C, r, c, 2.0 ** 2, 2.0 ** 8)
+    assert [i.stats.cg_iters for i in sol.iterations] == [pr.cg_iters for (*_, pr) in run.stages]
+    assert [i.gamma for i in sol.iterations] == [g for (_t, g, *_rest) in run.stages]
+    assert rel_inf(sol.final_state.u, run.state.u) <= 1e-10
+    assert rel_inf(sol.final_state.v, run.state.v) <= 1e-10
