@@ -148,37 +148,44 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
         }
       }
     } else if (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART) {
-      // 8 columns per lane per tile: chunk max, one rescale, then exps
+      // 8 columns per lane per tile: chunk max, one rescale, then exps; each
+      // staged column point is read once for all RW rows (column-outer loop)
+      double e[RW][8];
 #pragma unroll
-      for (int r = 0; r < RW; ++r) {
-        double e[8];
-        double cm = OTN_NINF;
+      for (int q = 0; q < 8; ++q) {
+        const int t = lane + 32 * q;
+        if (t < jn) {
+          double bb[D];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int t = lane + 32 * q;
-          if (t < jn) {
-            double bb[D];
+          for (int k = 0; k < D; ++k) bb[k] = sb[k][t];
+          const double cpt = scp[t];
 #pragma unroll
-            for (int k = 0; k < D; ++k) bb[k] = sb[k][t];
+          for (int r = 0; r < RW; ++r) {
             if (SEP) {
-              e[q] = sep_exponent<D>(a[r], bb, rp[r], scp[t], G);
+              e[r][q] = sep_exponent<D>(a[r], bb, rp[r], cpt, G);
             } else {
               const double c = pc_cost<D>(a[r], bb, p.cmax, rc);
-              e[q] = __dadd_rn(__dmul_rn(p.ng, c), scp[t]);
-              if (p.rowpot) e[q] = __dadd_rn(e[q], rp[r]);
+              e[r][q] = __dadd_rn(__dmul_rn(p.ng, c), cpt);
+              if (p.rowpot) e[r][q] = __dadd_rn(e[r][q], rp[r]);
             }
-          } else {
-            e[q] = OTN_NINF;
           }
-          cm = fmax(cm, e[q]);
+        } else {
+#pragma unroll
+          for (int r = 0; r < RW; ++r) e[r][q] = OTN_NINF;
         }
+      }
+#pragma unroll
+      for (int r = 0; r < RW; ++r) {
+        double cm = OTN_NINF;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cm = fmax(cm, e[r][q]);
         if (cm > m[r]) {
           s[r] = s[r] * exp_tab(m[r] - cm, s_exp);
           m[r] = cm;
         }
         if (m[r] != OTN_NINF) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) s[r] += exp_tab(e[q] - m[r], s_exp);
+          for (int q = 0; q < 8; ++q) s[r] += exp_tab(e[r][q] - m[r], s_exp);
         }
       }
     } else {
