@@ -272,15 +272,14 @@ static cudaError_t launch_rw(const PairArgs& p, cudaStream_t st, bool sep) {
 }
 
 // Rows per warp / CTAs per SM (measured on B200, d = 3, n = 65536, 8192..65536
-// rows): the log-sum-exp passes keep 8 exponents per row in flight, so they
-// run 2 rows per warp at 3 CTAs per SM; the product passes reuse each staged
-// column point across 4 rows per warp at 2 CTAs per SM, dropping to 2 rows
-// when that leaves SMs idle.  8 rows per warp spills (the previous choice,
-// 1.6-1.8x slower).
+// rows): the log-sum-exp and product passes reuse each staged column point
+// across 4 rows per warp at 2 CTAs per SM (LSE: 9.5 ms per pass against 9.9
+// with 2 rows at 3 CTAs per SM), dropping to 2 rows when that leaves SMs idle;
+// the shifted column LSE keeps 2 rows.  8 rows per warp spills (the first
+// choice, 1.6-1.8x slower).
 template <int D, int OP>
 static cudaError_t launch_d(const PairArgs& p, cudaStream_t st, int num_sms, bool sep) {
-  if (OP == OTN_PC_LSE || OP == OTN_PC_LSE_PART || OP == OTN_PC_LSE_SHIFT ||
-      (p.na + 31) / 32 < num_sms)
+  if (OP == OTN_PC_LSE_SHIFT || (p.na + 31) / 32 < num_sms)
     return launch_rw<2, D, OP, 3>(p, st, sep);
   return launch_rw<4, D, OP, 2>(p, st, sep);
 }
