@@ -125,22 +125,24 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
     __syncthreads();
     const int jn = int(p.nb - j0 < kPcTile ? p.nb - j0 : int64_t(kPcTile));
     if (OP == OTN_PC_LSE_SHIFT) {
-      // against the known shift: no running max, no rescale
+      // against the known shift: no running max, no rescale; each staged
+      // column point read once for all RW rows
 #pragma unroll
-      for (int r = 0; r < RW; ++r) {
+      for (int q = 0; q < 8; ++q) {
+        const int t = lane + 32 * q;
+        if (t < jn) {
+          double bb[D];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int t = lane + 32 * q;
-          if (t < jn) {
-            double bb[D];
+          for (int k = 0; k < D; ++k) bb[k] = sb[k][t];
+          const double cpt = scp[t];
 #pragma unroll
-            for (int k = 0; k < D; ++k) bb[k] = sb[k][t];
+          for (int r = 0; r < RW; ++r) {
             double e;
             if (SEP) {
-              e = sep_exponent<D>(a[r], bb, rp[r], scp[t], G);
+              e = sep_exponent<D>(a[r], bb, rp[r], cpt, G);
             } else {
               const double c = pc_cost<D>(a[r], bb, p.cmax, rc);
-              e = __dadd_rn(__dmul_rn(p.ng, c), scp[t]);
+              e = __dadd_rn(__dmul_rn(p.ng, c), cpt);
               if (p.rowpot) e = __dadd_rn(e, rp[r]);
             }
             s[r] += exp_tab(__dsub_rn(e, m[r]), s_exp);
@@ -274,12 +276,11 @@ static cudaError_t launch_rw(const PairArgs& p, cudaStream_t st, bool sep) {
 // Rows per warp / CTAs per SM (measured on B200, d = 3, n = 65536, 8192..65536
 // rows): the log-sum-exp and product passes reuse each staged column point
 // across 4 rows per warp at 2 CTAs per SM (LSE: 9.5 ms per pass against 9.9
-// with 2 rows at 3 CTAs per SM), dropping to 2 rows when that leaves SMs idle;
-// the shifted column LSE keeps 2 rows.  8 rows per warp spills (the first
-// choice, 1.6-1.8x slower).
+// with 2 rows at 3 CTAs per SM), dropping to 2 rows when that leaves SMs
+// idle.  8 rows per warp spills (the first choice, 1.6-1.8x slower).
 template <int D, int OP>
 static cudaError_t launch_d(const PairArgs& p, cudaStream_t st, int num_sms, bool sep) {
-  if (OP == OTN_PC_LSE_SHIFT || (p.na + 31) / 32 < num_sms)
+  if ((p.na + 31) / 32 < num_sms)
     return launch_rw<2, D, OP, 3>(p, st, sep);
   return launch_rw<4, D, OP, 2>(p, st, sep);
 }
