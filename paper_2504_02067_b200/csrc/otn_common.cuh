@@ -169,6 +169,12 @@ __device__ __forceinline__ double exp_tab(double x, const double2* __restrict__ 
   return exp_tab_nc(x < -746.0 ? -746.0 : (x > 710.0 ? 710.0 : x), tab);
 }
 
+// exp_tab for x <= 0 (a term against its running maximum): the upper clamp
+// cannot trigger, so it is dropped -- the same bits, NaN included.
+__device__ __forceinline__ double exp_tab_le0(double x, const double2* __restrict__ tab) {
+  return exp_tab_nc(x < -746.0 ? -746.0 : x, tab);
+}
+
 // s + exp(x) for x <= 0 (log-sum-exp accumulation against a running max):
 // entries below -746 add an exact 0 and are skipped; NaN propagates.
 __device__ __forceinline__ double add_exp_le0(double s, double x, const double2* __restrict__ tab) {

@@ -182,12 +182,12 @@ __global__ void __launch_bounds__(kPcThreads, MB) k_pair(PairArgs p) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) cm = fmax(cm, e[r][q]);
         if (cm > m[r]) {
-          s[r] = s[r] * exp_tab(m[r] - cm, s_exp);
+          s[r] = s[r] * exp_tab_le0(m[r] - cm, s_exp);
           m[r] = cm;
         }
         if (m[r] != OTN_NINF) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) s[r] += exp_tab(e[r][q] - m[r], s_exp);
+          for (int q = 0; q < 8; ++q) s[r] += exp_tab_le0(e[r][q] - m[r], s_exp);
         }
       }
     } else {
