@@ -24,6 +24,12 @@ __device__ __forceinline__ uint32_t ld_acq(const uint32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint32_t ld_rlx(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 struct Buf {
   double* red;        // [2][2][STR] doubles
   uint64_t* gs;       // [2][2][STR][2]
@@ -269,6 +275,63 @@ __device__ void red_cntk(const Buf& b, double* v, uint32_t& ep) {
   ep = e;
 }
 
+// variant 14/15/16: counter + loads (as 6, slot loads issued before the adds),
+// thread 0 polling with D relaxed loads in flight, issued S cycles apart, then
+// an acq_rel fence (17: D = 4 with ld.acquire polls, no fence)
+template <int D, int S, bool ACQ>
+__device__ void red_cnt_pipe(const Buf& b, double* v, uint32_t& ep) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x;
+  const uint32_t e = ep + 1;
+  double* base = b.red + (e & 1) * 2 * STR;
+  for (int k = 0; k < 2; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0) for (int k = 0; k < 2; ++k) s_red[k][warp] = v[k];
+  __syncthreads();
+  if (warp < 2) {
+    double t = warp_sum(lane < NW ? s_red[warp][lane] : 0.0);
+    if (lane == 0) __stcg(base + warp * STR + blockIdx.x, t);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(b.cnt) : "memory");
+    const uint32_t target = e * uint32_t(G);
+    uint32_t c[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      c[d] = ACQ ? ld_acq(b.cnt) : ld_rlx(b.cnt);
+      if (d + 1 < D) {
+        const long long t0 = clock64();
+        while (clock64() - t0 < S) {}
+      }
+    }
+    bool done = false;
+    while (!done) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        if (!done) {
+          if (int32_t(c[d] - target) >= 0) done = true;
+          else c[d] = ACQ ? ld_acq(b.cnt) : ld_rlx(b.cnt);
+        }
+      }
+    }
+    if (!ACQ) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp < 2) {
+    double2 p[STR / 64];
+    for (int m = 0; m < STR / 64; ++m) {
+      int bb = 64 * m + 2 * lane;
+      p[m] = bb < G ? __ldcg(reinterpret_cast<const double2*>(base + warp * STR + bb)) : make_double2(0, 0);
+    }
+    double t = 0.0;
+    for (int m = 0; m < STR / 64; ++m) t += p[m].x + p[m].y;
+    t = warp_sum(t);
+    if (lane == 0) s_res[warp] = t;
+  }
+  __syncthreads();
+  v[0] = s_res[0]; v[1] = s_res[1];
+  ep = e;
+}
+
 // variant 4: arrival counter; the last arriver sums and broadcasts (value + epoch) in one line
 __device__ void red_last(const Buf& b, double* v, uint32_t& ep) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x;
@@ -345,6 +408,12 @@ __global__ void __launch_bounds__(NT, 1) k(Buf b, int variant, int reps) {
     else if (variant == 11) red_cntk<4>(b, v, ep);
     else if (variant == 12) red_cntk<8>(b, v, ep);
     else if (variant == 13) red_cntk<16>(b, v, ep);
+    else if (variant == 14) red_cnt_pipe<1, 0, false>(b, v, ep);
+    else if (variant == 15) red_cnt_pipe<2, 300, false>(b, v, ep);
+    else if (variant == 16) red_cnt_pipe<4, 150, false>(b, v, ep);
+    else if (variant == 17) red_cnt_pipe<4, 150, true>(b, v, ep);
+    else if (variant == 18) red_cnt_pipe<8, 80, false>(b, v, ep);
+    else if (variant == 19) red_cnt_pipe<1, 0, true>(b, v, ep);
     else red_last(b, v, ep);
     acc += v[0] + v[1];
   }
@@ -364,8 +433,11 @@ int main() {
                          "counter (release red) + loads", "counter barrier only", "cg grid.sync only",
                          "warp 0: lane 0 spins", "warp 0: whole warp polls",
                          "counter over 4 lines + loads", "counter over 8 lines + loads",
-                         "counter over 16 lines + loads"};
-  for (int variant : {3, 11, 12, 13}) {
+                         "counter over 16 lines + loads",
+                         "pipe: 1 relaxed poll + fence", "pipe: 2 relaxed polls + fence",
+                         "pipe: 4 relaxed polls + fence", "pipe: 4 acquire polls",
+                         "pipe: 8 relaxed polls + fence", "pipe: 1 acquire poll (product)"};
+  for (int variant : {6, 19, 14, 15, 16, 17, 18}) {
     for (int rep = 0; rep < 3; ++rep) {
       cudaMemset(b.gs, 0, 2 * 2 * STR * 16);
       cudaMemset(b.cnt, 0, 32 * 4 * 16);
