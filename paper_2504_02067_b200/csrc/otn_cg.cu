@@ -1208,7 +1208,11 @@ __device__ __forceinline__ void publish_result(const CoopArgs& a, const DevResul
   }
 }
 
-__global__ void __launch_bounds__(NT, 1) k_coop(CoopArgs a) {
+// The arguments stay in the kernel's parameter space (__grid_constant__): the
+// device functions take them by reference, which would otherwise copy the
+// struct to local memory and turn every field read in the CG loop into a
+// local load (measured: D2 solve 73.1 -> 70.3 ms, bit-identical).
+__global__ void __launch_bounds__(NT, 1) k_coop(const __grid_constant__ CoopArgs a) {
   __shared__ Smem sh;
   cg::grid_group grid = cg::this_grid();
   const int G = gridDim.x;
