@@ -174,6 +174,7 @@ enum PlanMode { kPlanRing = 0, kPlanL2 = 1, kPlanSparse = 2, kPlanSparseG = 3 };
 __shared__ int s_mode;
 __shared__ int s_nzc;                               // kPlanSparse: nonempty columns of the CTA
 __shared__ int s_split;                             // kPlanSparse: threads splitting the CSC entries
+__shared__ int s_direct2;                           // kPlanSparse: this CTA stores its CSC values directly
 __shared__ uint16_t s_m0[kCoopThreads];             // kPlanSparse: column of each thread's first entry
 __shared__ int s_kb[kCoopThreads + 1];              // kPlanSparse: first CSC entry of each thread
 
@@ -382,9 +383,10 @@ struct SparseView {
   uint32_t* perm;                                   // mode 2: CSC slot -> CSR entry | row << 16
   double* cval;                                     // mode 3: CSC values
   uint16_t* crow;                                   // mode 3: CSC rows
-  double* scval;                                    // mode 3: CSC slots [0, kSparseGS) in shared memory
+  double* scval;                                    // CSC slots [0, gs) in shared memory
   uint16_t* scrow;
-  bool direct;                                      // mode 3
+  int gs;                                           // slots held in shared memory
+  bool direct;                                      // mode 3, or mode 2 with few nonzeros
 };
 
 // Mode 3 keeps the first kSparseGS slots of its (thread-interleaved) CSC in
@@ -392,6 +394,17 @@ struct SparseView {
 // first entries, read without an L2 round trip -- past the staged spans.
 constexpr size_t kSparseGSmem = (kSparseVal + size_t(kSparseRows) * 4 + 15) / 16 * 16;
 constexpr int kSparseGS = int((kSparseBytes + size_t(kSparseRows) * 4 - kSparseGSmem) / 10) / 8 * 8;
+
+// Mode 2 with at most kSparseDCap nonzeros stores its CSC values and rows
+// directly (like mode 3, all slots in shared memory: no CSR-entry indirection,
+// contiguous reads in phase A), in the same region: CSR values + columns
+// [kSparseDCap], then CSC values + rows [kSparseDCap + NT] (interleaving slack).
+constexpr int kSparseDCap = int((kSparseCap * 14 - 10 * kCoopThreads) / 20);
+constexpr size_t kSparseDCol = kSparseVal + size_t(kSparseDCap) * 8;
+constexpr size_t kSparseDSv = kSparseDCol + size_t(kSparseDCap) * 2;
+constexpr size_t kSparseDSr = kSparseDSv + size_t(kSparseDCap + kCoopThreads) * 8;
+static_assert(kSparseDSr + size_t(kSparseDCap + kCoopThreads) * 2 <= kSparseBytes,
+              "mode-2 direct CSC fits the compressed-rows region");
 
 // Per-CTA slice of the global compressed-rows buffer (kPlanSparseG):
 // val [cap] + cval [slot] doubles, then col [cap] + crow [slot] u16.
@@ -414,6 +427,17 @@ __device__ __forceinline__ SparseView sparse_view(void* sg) {
     v.perm = nullptr;
     v.scval = reinterpret_cast<double*>(b + kSparseGSmem);
     v.scrow = reinterpret_cast<uint16_t*>(b + kSparseGSmem + size_t(kSparseGS) * 8);
+    v.gs = kSparseGS;
+    v.direct = true;
+  } else if (s_direct2) {
+    v.val = reinterpret_cast<double*>(b + kSparseVal);
+    v.col = reinterpret_cast<uint16_t*>(b + kSparseDCol);
+    v.perm = nullptr;
+    v.cval = nullptr;
+    v.crow = nullptr;
+    v.scval = reinterpret_cast<double*>(b + kSparseDSv);
+    v.scrow = reinterpret_cast<uint16_t*>(b + kSparseDSr);
+    v.gs = 1 << 30;
     v.direct = true;
   } else {
     v.val = reinterpret_cast<double*>(b + kSparseVal);
@@ -423,6 +447,7 @@ __device__ __forceinline__ SparseView sparse_view(void* sg) {
     v.crow = nullptr;
     v.scval = nullptr;
     v.scrow = nullptr;
+    v.gs = 0;
     v.direct = false;
   }
   return v;
@@ -463,7 +488,9 @@ __device__ void block_incl_scan(int* a, int len, Smem& sh) {
 
 // Extract this CTA's nonzeros (CSR, column order) and build the local CSC.
 __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* wrow, Smem& sh) {
-  const SparseView sp = sparse_view(a.sg);
+  if (threadIdx.x == 0) s_direct2 = 0;
+  __syncthreads();
+  SparseView sp = sparse_view(a.sg);
   const PlanView v = plan_view(a, r0, r1);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int rows = int(r1 - r0);
@@ -476,9 +503,13 @@ __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* 
       if (r < rows) sp.rp[r + 1] = run + incl;
       run += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (lane == 0) sp.rp[0] = 0;
+    if (lane == 0) {
+      sp.rp[0] = 0;
+      if (s_mode == kPlanSparse && run <= kSparseDCap) s_direct2 = 1;
+    }
   }
   __syncthreads();
+  sp = sparse_view(a.sg);                           // the layout s_direct2 selects
   const unsigned lt = (1u << lane) - 1u;
   constexpr int U = 8;                              // 64-column steps loaded at once
   for (int r = warp; r < rows; r += NW) {           // warp per row, columns ascending
@@ -542,7 +573,7 @@ __device__ void stage_sparse(const CoopArgs& a, int64_t r0, int64_t r1, double* 
         while (s_kb[o] > k) --o;
         const int addr = (k - s_kb[o]) * split + o;
         if (sp.direct) {
-          if (addr < kSparseGS) {
+          if (addr < sp.gs) {
             sp.scval[addr] = sp.val[e];
             sp.scrow[addr] = uint16_t(r);
           } else {
@@ -674,8 +705,8 @@ __device__ void phase_a_sparse(void* sg, int64_t r0, int64_t r1, double* wrow, S
     };
     int k0 = kb;
     if (sp.direct) {
-      // this thread's slots (k - kb) * S + t below kSparseGS sit in shared memory
-      const int ks = t < kSparseGS ? min(ke, kb + (kSparseGS - 1 - t) / S + 1) : kb;
+      // this thread's slots (k - kb) * S + t below sp.gs sit in shared memory
+      const int ks = t < sp.gs ? min(ke, kb + (sp.gs - 1 - t) / S + 1) : kb;
       for (; k0 < ks; k0 += 8) batch(k0, ks, std::true_type{});
       k0 = ks;
     }
