@@ -332,6 +332,46 @@ __device__ void red_cnt_pipe(const Buf& b, double* v, uint32_t& ep) {
   ep = e;
 }
 
+// variant 20/21: the product's exchange (acquire poll, loads before the adds)
+// with each CTA's slot padded to its own 32-byte sector (20) / 128-byte line (21)
+// (no write sharing of slot lines between CTAs)
+template <int PAD>
+__device__ void red_cnt_pad(const Buf& b, double* v, uint32_t& ep) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x;
+  const uint32_t e = ep + 1;
+  double* base = b.red + (e & 1) * 2 * STR * PAD;
+  for (int k = 0; k < 2; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0) for (int k = 0; k < 2; ++k) s_red[k][warp] = v[k];
+  __syncthreads();
+  if (warp < 2) {
+    double t = warp_sum(lane < NW ? s_red[warp][lane] : 0.0);
+    if (lane == 0) __stcg(base + (warp * STR + blockIdx.x) * PAD, t);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(b.cnt) : "memory");
+    const uint32_t target = e * uint32_t(G);
+    while (int32_t(ld_acq(b.cnt) - target) < 0) {}
+  }
+  __syncthreads();
+  if (warp < 2) {
+    double p[STR / 32];
+#pragma unroll
+    for (int m = 0; m < STR / 32; ++m) {
+      const int bb = 32 * m + lane;
+      p[m] = bb < G ? __ldcg(base + (warp * STR + bb) * PAD) : 0.0;
+    }
+    double t = 0.0;
+#pragma unroll
+    for (int m = 0; m < STR / 32; ++m) t += p[m];
+    t = warp_sum(t);
+    if (lane == 0) s_res[warp] = t;
+  }
+  __syncthreads();
+  v[0] = s_res[0]; v[1] = s_res[1];
+  ep = e;
+}
+
 // variant 4: arrival counter; the last arriver sums and broadcasts (value + epoch) in one line
 __device__ void red_last(const Buf& b, double* v, uint32_t& ep) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x;
@@ -414,6 +454,8 @@ __global__ void __launch_bounds__(NT, 1) k(Buf b, int variant, int reps) {
     else if (variant == 17) red_cnt_pipe<4, 150, true>(b, v, ep);
     else if (variant == 18) red_cnt_pipe<8, 80, false>(b, v, ep);
     else if (variant == 19) red_cnt_pipe<1, 0, true>(b, v, ep);
+    else if (variant == 20) red_cnt_pad<4>(b, v, ep);
+    else if (variant == 21) red_cnt_pad<16>(b, v, ep);
     else red_last(b, v, ep);
     acc += v[0] + v[1];
   }
@@ -424,7 +466,7 @@ int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   Buf b;
-  cudaMalloc(&b.red, 2 * 2 * STR * 8);
+  cudaMalloc(&b.red, 2 * 2 * STR * 8 * 16);
   cudaMalloc(&b.gs, 2 * 2 * STR * 16);
   cudaMalloc(&b.cnt, 32 * 4 * 16);
   cudaMalloc(&b.out, 64);
@@ -436,8 +478,9 @@ int main() {
                          "counter over 16 lines + loads",
                          "pipe: 1 relaxed poll + fence", "pipe: 2 relaxed polls + fence",
                          "pipe: 4 relaxed polls + fence", "pipe: 4 acquire polls",
-                         "pipe: 8 relaxed polls + fence", "pipe: 1 acquire poll (product)"};
-  for (int variant : {6, 19, 14, 15, 16, 17, 18}) {
+                         "pipe: 8 relaxed polls + fence", "pipe: 1 acquire poll (product)",
+                         "product, slots padded to 32 B", "product, slots padded to 128 B"};
+  for (int variant : {19, 20, 21}) {
     for (int rep = 0; rep < 3; ++rep) {
       cudaMemset(b.gs, 0, 2 * 2 * STR * 16);
       cudaMemset(b.cnt, 0, 32 * 4 * 16);
